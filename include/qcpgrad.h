@@ -1,0 +1,151 @@
+/* qcpgrad -- B200-native derivative/adjoint of the QCP solution map.
+ *
+ * C ABI of libqcpgrad.so (paper_2508_17522_b200/_lib/libqcpgrad.so).  Plain
+ * pointers and sizes only.  Unless stated otherwise every array argument is a
+ * DEVICE pointer (cudaMalloc / torch CUDA storage) owned by the caller; cone
+ * block tables and size arrays are HOST pointers.  `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  Every call returns a qg_status; the
+ * message of the last failure on the calling thread is qg_last_error().
+ *
+ * Reference interfaces replaced (paths relative to the reference's
+ * pkg/src/conegrad/):
+ *   qg_create / qg_create_batch  <- ProblemData + embed + _embedding_project +
+ *                                   make_F preparation (embedding.py:59-115,
+ *                                   337-427; solution_map.py:170-179)
+ *   qg_jvp                       <- solution_map.jvp   (solution_map.py:325-355)
+ *   qg_vjp                       <- solution_map.vjp   (solution_map.py:358-385)
+ *   qg_apply_F                   <- make_F(...).matvec / .rmatvec
+ *                                   (embedding.py:420-425)
+ *   qg_check                     <- check_solution     (solution_map.py:263-288)
+ *   qg_cones_*                   <- cones.project / project_dual /
+ *                                   dprojection(_dual).matvec (cones.py:926-963)
+ *   qg_spmv_csc                  <- _kernels.spmv / spmv_adjoint backend slot
+ *                                   (_kernels/__init__.py:23-50, _csc.pyx:17-50)
+ */
+#ifndef QCPGRAD_H
+#define QCPGRAD_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes mirror the reference exception taxonomy (errors.py:13-38). */
+typedef enum {
+  QG_OK = 0,
+  QG_ERR_VALIDATION = 1,        /* ValidationError                          */
+  QG_ERR_DOMAIN = 2,            /* DomainError (tau <= 0, z_N <= 0)          */
+  QG_ERR_NUMERICAL = 3,         /* NumericalError (root finding, non-finite) */
+  QG_ERR_NOT_DIFFERENTIABLE = 4,/* NotDifferentiableError (pow apex)        */
+  QG_ERR_CUDA = 5,              /* CUDA runtime failure                     */
+  QG_ERR_UNSUPPORTED = 6        /* outside this build's limits              */
+} qg_status;
+
+/* Cone kinds in the reference's canonical order (cones.py:36-46). */
+typedef enum {
+  QG_CONE_ZERO = 0, QG_CONE_NONNEG = 1, QG_CONE_SOC = 2, QG_CONE_PSD = 3,
+  QG_CONE_EXP = 4, QG_CONE_DEXP = 5, QG_CONE_POW = 6, QG_CONE_DPOW = 7
+} qg_cone_kind;
+
+typedef struct {
+  int32_t kind;   /* qg_cone_kind                                  */
+  int32_t dim;    /* vectorised length (psd: order*(order+1)/2)    */
+  int32_t order;  /* psd matrix order, else 0                      */
+  double alpha;   /* pow/dpow exponent in (0,1), else 0            */
+} qg_cone_block;
+
+/* A batch of independent problems, concatenated in problem order.  Sparse
+ * matrices are CSC with int64 indices exactly as the reference stores them
+ * (sparse.py:19-73), each problem's col_ptr starting at 0.  P carries both
+ * triangles and is validated symmetric by the caller (sparse.py:173-194). */
+typedef struct {
+  int64_t nprob;
+  const int64_t *n, *m;           /* host [nprob]                         */
+  const int64_t *P_nnz, *A_nnz;   /* host [nprob]                         */
+  const int64_t *nblocks;         /* host [nprob]                         */
+  const qg_cone_block *blocks;    /* host, concatenated                    */
+  const int64_t *P_colptr, *P_rowidx; const double *P_vals; /* device      */
+  const int64_t *A_colptr, *A_rowidx; const double *A_vals; /* device      */
+  const double *q, *b;            /* device, sum(n) / sum(m)              */
+  const double *x, *y, *s;        /* device, sum(n) / sum(m) / sum(m)     */
+} qg_batch_desc;
+
+/* Perturbation (dP, dA, dq, db) for qg_jvp: CSC per problem, concatenated.
+ * same_pattern != 0 promises dP/dA share P's/A's exact patterns (the common
+ * case), which lets the kernels reuse the prepared transposes. */
+typedef struct {
+  const int64_t *dP_nnz, *dA_nnz;                            /* host [nprob] */
+  const int64_t *dP_colptr, *dP_rowidx; const double *dP_vals; /* device     */
+  const int64_t *dA_colptr, *dA_rowidx; const double *dA_vals; /* device     */
+  const double *dq, *db;                                       /* device     */
+  int32_t same_pattern;
+} qg_perturbation;
+
+typedef struct {
+  double atol, btol;   /* lsmr.py:57 defaults 1e-10                      */
+  int64_t max_iter;    /* 0 -> 10*(in_dim+out_dim) (lsmr.py:69-70);
+                          < 0 -> no iterations (explicit cap of zero)     */
+} qg_lsmr_opts;
+
+/* Per-problem diagnostics (solution_map.py:139-167, 313-322). */
+typedef struct {
+  int64_t iterations;
+  int32_t converged;
+  int32_t derivative_unreliable;
+  double residual_norm;   /* LSMR recurrence estimate normr (lsmr.py:161) */
+  double atr_norm;
+  double rhs_norm;
+} qg_diag;
+
+typedef struct qg_handle qg_handle;
+typedef struct qg_cones qg_cones;
+
+const char *qg_last_error(void);
+const char *qg_version(void);
+
+/* Prepare a batch: CSC->CSR transposes, z = (x, y-s, 1), Pi_K*(z) and the
+ * prepared projection derivative, P xbar and xbar'P xbar. */
+int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream);
+int qg_destroy(qg_handle *h);
+int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_t *total_m);
+
+/* jvp: outputs dx (sum n), dy, ds (sum m), diag[nprob] (host). */
+int qg_jvp(qg_handle *h, const qg_perturbation *dtheta, const qg_lsmr_opts *opts,
+           double *dx, double *dy, double *ds, qg_diag *diag, void *stream);
+/* vjp: inputs dx, dy, ds; outputs dP values (sum P_nnz, CSC order of P),
+ * dA values (CSC order of A), dq, db; diag[nprob] (host). */
+int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds,
+           const qg_lsmr_opts *opts, double *dP_vals, double *dA_vals, double *dq,
+           double *db, qg_diag *diag, void *stream);
+
+/* One operator application F w (transpose=0) or F' w (transpose=1) on the
+ * batch embedding vector laid out as [X (sum n) | Y (sum m) | T (nprob)]. */
+int qg_apply_F(qg_handle *h, int transpose, const double *w, double *out, void *stream);
+/* The projected embedding point Pi z in the same layout. */
+int qg_embedding_point(qg_handle *h, double *pz, void *stream);
+
+/* KKT residuals of (x, y, s) per problem: report[5*p + {primal,
+ * stationarity, gap, primal_cone_distance, dual_cone_distance}] (host). */
+int qg_check(qg_handle *h, const double *x, const double *y, const double *s, double *report, void *stream);
+
+/* Standalone cone calculus over a block table (host). */
+int qg_cones_create(qg_cones **out, const qg_cone_block *blocks, int64_t nblocks, void *stream);
+int qg_cones_destroy(qg_cones *c);
+int qg_cones_project(qg_cones *c, int dual, const double *z, double *out, void *stream);
+/* Prepare D Pi at z (dual or primal); subsequent applies reuse it. */
+int qg_cones_prepare(qg_cones *c, int dual, const double *z, void *stream);
+int qg_cones_apply(qg_cones *c, const double *dz, double *out, void *stream);
+
+/* Plain CSC products with int64 indices (the reference's SpMV backend slot). */
+int qg_spmv_csc(int64_t nrows, int64_t ncols, const int64_t *col_ptr, const int64_t *row_idx,
+                const double *values, int64_t nnz, int adjoint, const double *x, double *out,
+                void *stream);
+
+/* Number of kernels this library launched since load (telemetry). */
+int64_t qg_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QCPGRAD_H */

@@ -1,0 +1,582 @@
+// C ABI of libqcpgrad (include/qcpgrad.h): batch preparation, jvp / vjp
+// pipelines and the LSMR driver loop.
+//
+// Pipelines (reference solution_map.py:325-385):
+//   jvp: rhs = -D_theta Q(Pi z)[dtheta]/|z_N| -> LSMR(F, rhs) -> D phi(z)[dz]
+//   vjp: dz = D phi(z)'[delta] -> LSMR(F', -dz) -> D_theta Q(Pi z)'[w] on patterns
+// The loop runs in CUDA graphs of 4/16/64 iterations; every kernel reads a
+// per-problem active flag so converged problems cost no memory traffic.
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "operator.h"
+
+namespace qg {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void set_error(int, const std::string &msg) { g_last_error = msg; }
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+void count_launch(int n) { g_launches += n; }
+
+void Workspace::release() {
+  dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
+  dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
+  dev_free(st); dev_free(d_nactive);
+  if (h_nactive) cudaFreeHost(h_nactive);
+}
+
+struct GraphCache {
+  std::map<std::pair<int, int>, cudaGraphExec_t> exec;
+  ~GraphCache() {
+    for (auto &kv : exec) cudaGraphExecDestroy(kv.second);
+  }
+};
+static std::map<const Handle *, GraphCache *> g_graphs;
+static std::mutex g_graph_mu;
+
+Handle::~Handle() {
+  P.release(); Pc.release(); A.release(); AT.release();
+  dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
+  dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
+  ws.release();
+  std::lock_guard<std::mutex> g(g_graph_mu);
+  auto it = g_graphs.find(this);
+  if (it != g_graphs.end()) {
+    delete it->second;
+    g_graphs.erase(it);
+  }
+}
+
+static int pick_group(int64_t nnz, int64_t rows) {
+  if (rows <= 0) return 1;
+  const double avg = (double)nnz / (double)rows;
+  int g = 1;
+  while (g < 32 && g < avg * 0.75) g <<= 1;
+  return g;
+}
+
+// ------------------------------------------------------------ create ----
+static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
+  const int B = (int)d.nprob;
+  if (B <= 0) throw Error{QG_ERR_VALIDATION, "batch must hold at least one problem"};
+  H.B = B;
+  H.n.assign(d.n, d.n + B);
+  H.m.assign(d.m, d.m + B);
+  H.nnzP.assign(d.P_nnz, d.P_nnz + B);
+  H.nnzA.assign(d.A_nnz, d.A_nnz + B);
+  H.xoff.assign(B + 1, 0);
+  H.yoff.assign(B + 1, 0);
+  H.noffP.assign(B + 1, 0);
+  H.noffA.assign(B + 1, 0);
+  for (int p = 0; p < B; ++p) {
+    if (H.n[p] < 0 || H.m[p] < 0) throw Error{QG_ERR_VALIDATION, "negative problem dimension"};
+    H.xoff[p + 1] = H.xoff[p] + H.n[p];
+    H.yoff[p + 1] = H.yoff[p] + H.m[p];
+    H.noffP[p + 1] = H.noffP[p] + H.nnzP[p];
+    H.noffA[p + 1] = H.noffA[p] + H.nnzA[p];
+  }
+  H.NX = H.xoff[B];
+  H.NY = H.yoff[B];
+  H.NE = H.NX + H.NY + B;
+
+  // sparse structures
+  CscBatch cp{d.P_colptr, d.P_rowidx, d.P_vals, H.n, H.n, H.nnzP};
+  csc_to_csr(cp, H.P, &H.Pc, true, st);
+  CscBatch ca{d.A_colptr, d.A_rowidx, d.A_vals, H.n, H.m, H.nnzA};
+  csc_to_csr(ca, H.A, &H.AT, true, st);
+  H.AT.val = dev_alloc<double>(H.noffA[B]);
+  if (H.noffA[B])
+    QG_CUDA(cudaMemcpyAsync(H.AT.val, d.A_vals, sizeof(double) * H.noffA[B], cudaMemcpyDeviceToDevice, st));
+
+  // row-length statistics for the group sizes and unit partition
+  std::vector<int32_t> rpP(H.NX + 1), rpAT(H.NX + 1), rpA(H.NY + 1);
+  QG_CUDA(cudaMemcpyAsync(rpP.data(), H.P.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpAT.data(), H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpA.data(), H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnzX = (int64_t)rpP[H.NX] + rpAT[H.NX], nnzY = rpA[H.NY];
+  H.gx = pick_group(nnzX, H.NX);
+  H.gy = pick_group(nnzY, H.NY);
+  // aim for >= 4 CTAs per SM when the batch is large enough, 2k..16k entries per unit
+  const int64_t total = nnzX + nnzY + H.NX + H.NY;
+  int64_t target_nnz = std::max<int64_t>(2048, std::min<int64_t>(16384, total / (4 * 148) + 1));
+  const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
+  const int64_t target_rows_y = std::max<int64_t>(32, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
+
+  // X units: nnz-balanced row ranges within each problem
+  H.xunit_ptr.assign(B + 1, 0);
+  for (int p = 0; p < B; ++p) {
+    H.xunit_ptr[p] = (int64_t)H.xunits.size();
+    int64_t r = H.xoff[p];
+    const int64_t end = H.xoff[p + 1];
+    while (r < end) {
+      int64_t e = r, w = 0;
+      while (e < end && (e == r || (w < target_nnz && e - r < 4096))) {
+        w += (int64_t)(rpP[e + 1] - rpP[e]) + (rpAT[e + 1] - rpAT[e]) + 1;
+        ++e;
+      }
+      H.xunits.push_back(Unit{p, (int32_t)r, (int32_t)e, 0, 0, CLS_ELEM});
+      r = e;
+    }
+  }
+  H.xunit_ptr[B] = (int64_t)H.xunits.size();
+  H.d_xunits = dev_alloc<Unit>(H.xunits.size());
+  if (!H.xunits.empty())
+    QG_CUDA(cudaMemcpyAsync(H.d_xunits, H.xunits.data(), sizeof(Unit) * H.xunits.size(), cudaMemcpyHostToDevice, st));
+
+  // cones and Y units
+  std::vector<std::vector<qg_cone_block>> per(B);
+  int64_t bi = 0;
+  for (int p = 0; p < B; ++p) {
+    per[p].assign(d.blocks + bi, d.blocks + bi + d.nblocks[p]);
+    bi += d.nblocks[p];
+  }
+  H.cones.build(per, H.yoff, target_rows_y, st);
+  H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
+  H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
+  QG_CUDA(cudaMemcpyAsync(H.d_xunit_ptr, H.xunit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(H.d_yunit_ptr, H.cones.unit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+
+  // problem vectors
+  H.q = dev_alloc<double>(H.NX);
+  H.b = dev_alloc<double>(H.NY);
+  H.xbar = dev_alloc<double>(H.NX);
+  H.ybar = dev_alloc<double>(H.NY);
+  H.sbar = dev_alloc<double>(H.NY);
+  H.Pxbar = dev_alloc<double>(H.NX);
+  H.emb = dev_alloc<Embed>(B);
+  if (H.NX) {
+    QG_CUDA(cudaMemcpyAsync(H.q, d.q, sizeof(double) * H.NX, cudaMemcpyDeviceToDevice, st));
+    QG_CUDA(cudaMemcpyAsync(H.xbar, d.x, sizeof(double) * H.NX, cudaMemcpyDeviceToDevice, st));
+  }
+  if (H.NY) QG_CUDA(cudaMemcpyAsync(H.b, d.b, sizeof(double) * H.NY, cudaMemcpyDeviceToDevice, st));
+
+  // workspace
+  Workspace &W = H.ws;
+  W.u = dev_alloc<double>(H.NE); W.v = dev_alloc<double>(H.NE); W.h = dev_alloc<double>(H.NE);
+  W.hb = dev_alloc<double>(H.NE); W.x = dev_alloc<double>(H.NE);
+  W.dpu = dev_alloc<double>(H.NY); W.dpv = dev_alloc<double>(H.NY);
+  W.tY = dev_alloc<double>(H.NY); W.tY2 = dev_alloc<double>(H.NY);
+  W.part = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
+  W.st = dev_alloc<Lsmr>(B);
+  W.d_nactive = dev_alloc<int>(1);
+  QG_CUDA(cudaMallocHost(&W.h_nactive, sizeof(int)));
+
+  // embedding: z = (x, y - s, 1); Pi z; D Pi prep; P xbar, xbar'P xbar
+  double *zmid = H.cones.d_zmid;
+  launch_embed_prep(H, d.x, d.y, d.s, zmid, st);
+  H.cones.prepare(zmid, H.ybar, 1, true, st);
+  H.cones.check_errors(st);
+  Mats M = make_mats(H);
+  launch_embed_consts(H, M, W.part, st);
+}
+
+}  // namespace qg
+
+// sbar = ybar - zmid (solution_map.py:223): tiny kernel kept local
+namespace qg {
+__global__ void k_sub(const double *a, const double *b, double *out, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i] - b[i];
+}
+static void launch_sub(const double *a, const double *b, double *out, int64_t n, cudaStream_t st) {
+  if (n <= 0) return;
+  k_sub<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, b, out, n);
+  QG_LAUNCHED();
+}
+
+// ----------------------------------------------------------- LSMR loop --
+struct LoopVecs {
+  int ku, kv;
+};
+
+static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
+  Workspace &W = H.ws;
+  const int ku = jvp ? STEP_F : STEP_FT, kv = jvp ? STEP_FT : STEP_F;
+  for (int i = 0; i < iters; ++i) {
+    StepArgs su{W.v, W.dpv, W.u, W.u, ku == STEP_FT ? W.dpu : nullptr, W.tY, W.tY2, W.st, 0, W.part};
+    launch_step(H, M, ku, su, st);
+    FinArgs fu{H.B, PH_STEP_U, ku, W.st, W.part, W.v, W.u, W.u, W.h, W.hb, W.x, W.v};
+    launch_fin(H, M, fu, st);
+    StepArgs sv{W.u, W.dpu, W.v, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 1, W.part};
+    launch_step(H, M, kv, sv, st);
+    FinArgs fv{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
+    launch_fin(H, M, fv, st);
+    UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
+    launch_update(H, M, ua, st);
+    FinArgs fx{H.B, PH_STEP_X, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
+    launch_fin(H, M, fx, st);
+  }
+}
+
+static cudaGraphExec_t get_graph(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
+  GraphCache *gc;
+  {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    auto it = g_graphs.find(&H);
+    if (it == g_graphs.end()) it = g_graphs.emplace(&H, new GraphCache()).first;
+    gc = it->second;
+  }
+  auto key = std::make_pair(jvp ? 1 : 0, iters);
+  auto it = gc->exec.find(key);
+  if (it != gc->exec.end()) return it->second;
+  cudaStream_t cs;
+  QG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t graph;
+  QG_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const long long before = g_launches.load();
+  try {
+    capture_iters(H, M, jvp, iters, cs);
+  } catch (...) {
+    cudaStreamEndCapture(cs, &graph);
+    cudaStreamDestroy(cs);
+    throw;
+  }
+  g_launches = before;  // captured launches are counted when the graph runs
+  QG_CUDA(cudaStreamEndCapture(cs, &graph));
+  cudaGraphExec_t exec;
+  QG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  gc->exec[key] = exec;
+  (void)st;
+  return exec;
+}
+
+static int kernels_per_iter(const Handle &H) {
+  return 6 - (H.nxu() + H.nyu() == 0 ? 3 : 0);
+}
+
+static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
+  Workspace &W = H.ws;
+  long long done = 0;
+  while (true) {
+    launch_count_active(H, st);
+    QG_CUDA(cudaMemcpyAsync(W.h_nactive, W.d_nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+    QG_CUDA(cudaStreamSynchronize(st));
+    if (*W.h_nactive == 0 || done >= cap) break;
+    const long long rem = cap - done;
+    const int g = rem >= 64 ? 64 : (rem >= 16 ? 16 : (rem >= 4 ? 4 : 1));
+    cudaGraphExec_t ex = get_graph(H, M, jvp, g, st);
+    QG_CUDA(cudaGraphLaunch(ex, st));
+    count_launch(g * kernels_per_iter(H));
+    done += g;
+  }
+}
+
+static void lsmr_begin(Handle &H, const qg_lsmr_opts &o, cudaStream_t st, long long &cap) {
+  std::vector<long long> mi(H.B);
+  cap = 0;
+  for (int p = 0; p < H.B; ++p) {
+    const long long N = H.n[p] + H.m[p] + 1;
+    // lsmr.py:69-70: None -> 10 * (in + out); the ABI encodes None as 0 and an
+    // explicit cap of zero as a negative value
+    mi[p] = (o.max_iter > 0) ? o.max_iter : (o.max_iter < 0 ? 0 : 20 * N);
+    cap = std::max(cap, mi[p]);
+  }
+  long long *d_mi = dev_alloc<long long>(H.B);
+  QG_CUDA(cudaMemcpyAsync(d_mi, mi.data(), sizeof(long long) * H.B, cudaMemcpyHostToDevice, st));
+  launch_init_state(H, o.atol, o.btol, d_mi, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  dev_free(d_mi);
+  Workspace &W = H.ws;
+  QG_CUDA(cudaMemsetAsync(W.x, 0, sizeof(double) * H.NE, st));
+  QG_CUDA(cudaMemsetAsync(W.h, 0, sizeof(double) * H.NE, st));
+  QG_CUDA(cudaMemsetAsync(W.hb, 0, sizeof(double) * H.NE, st));
+}
+
+static void lsmr_finish(Handle &H, qg_diag *diag, cudaStream_t st) {
+  std::vector<Lsmr> L(H.B);
+  QG_CUDA(cudaMemcpyAsync(L.data(), H.ws.st, sizeof(Lsmr) * H.B, cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  for (int p = 0; p < H.B; ++p) {
+    if (L[p].status) {
+      throw Error{QG_ERR_NUMERICAL, (H.B > 1 ? "problem " + std::to_string(p) + ": " : std::string()) +
+                                        "non-finite quantity in LSMR at iteration " + std::to_string(L[p].itn)};
+    }
+    if (diag) {
+      diag[p].iterations = L[p].itn;
+      diag[p].converged = L[p].converged;
+      diag[p].residual_norm = L[p].normr;
+      diag[p].atr_norm = L[p].normar;
+      diag[p].rhs_norm = L[p].normb;
+      diag[p].derivative_unreliable = L[p].normr > 1e-6 * L[p].normb;   // solution_map.py:314
+    }
+  }
+}
+
+// After the rhs is in W.u (and, for vjp, D Pi(u_Y) in W.dpu): initial
+// v = OP'(u)/beta, alpha, h = v, hbar = x = 0 (lsmr.py:72-103), then loop.
+static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long long cap, cudaStream_t st) {
+  Workspace &W = H.ws;
+  FinArgs fr{H.B, PH_RHS, rhs_kind, W.st, W.part, W.u, nullptr, W.u, W.h, W.hb, W.x, W.v};
+  launch_fin(H, M, fr, st);
+  const int kv = jvp ? STEP_FT : STEP_F;
+  StepArgs s0{W.u, W.dpu, nullptr, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 0, W.part};
+  launch_step(H, M, kv, s0, st);
+  FinArgs f0{H.B, PH_INIT_V, kv, W.st, W.part, W.u, nullptr, W.v, W.h, W.hb, W.x, W.v};
+  launch_fin(H, M, f0, st);
+  UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
+  launch_update(H, M, ua, st);
+  run_lsmr_loop(H, M, jvp, cap, st);
+}
+
+}  // namespace qg
+
+using namespace qg;
+
+#define QG_API_BEGIN try {
+#define QG_API_END                                                     \
+  return QG_OK;                                                        \
+  }                                                                    \
+  catch (const qg::Error &e) { return qg::fail(e.code, e.msg); }        \
+  catch (const std::exception &e) { return qg::fail(QG_ERR_CUDA, e.what()); }
+
+extern "C" {
+
+const char *qg_last_error(void) { return g_last_error.c_str(); }
+const char *qg_version(void) { return "qcpgrad 0.1.0 (sm_100a)"; }
+int64_t qg_kernel_launches(void) { return g_launches.load(); }
+
+int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream) {
+  QG_API_BEGIN
+  cudaStream_t st = (cudaStream_t)stream;
+  auto *H = new Handle();
+  try {
+    build_handle(*H, *desc, st);
+    launch_sub(H->ybar, H->cones.d_zmid, H->sbar, H->NY, st);
+    QG_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    delete H;
+    throw;
+  }
+  *out = reinterpret_cast<qg_handle *>(H);
+  QG_API_END
+}
+
+int qg_destroy(qg_handle *h) {
+  QG_API_BEGIN
+  delete reinterpret_cast<Handle *>(h);
+  QG_API_END
+}
+
+int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_t *total_m) {
+  QG_API_BEGIN
+  const Handle *H = reinterpret_cast<const Handle *>(h);
+  *nprob = H->B;
+  *total_n = H->NX;
+  *total_m = H->NY;
+  QG_API_END
+}
+
+int qg_embedding_point(qg_handle *h, double *pz, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (H.NX) QG_CUDA(cudaMemcpyAsync(pz, H.xbar, sizeof(double) * H.NX, cudaMemcpyDeviceToDevice, st));
+  if (H.NY) QG_CUDA(cudaMemcpyAsync(pz + H.NX, H.ybar, sizeof(double) * H.NY, cudaMemcpyDeviceToDevice, st));
+  std::vector<Embed> E(H.B);
+  QG_CUDA(cudaMemcpyAsync(E.data(), H.emb, sizeof(Embed) * H.B, cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  std::vector<double> t(H.B);
+  for (int p = 0; p < H.B; ++p) t[p] = E[p].tau;
+  QG_CUDA(cudaMemcpyAsync(pz + H.NX + H.NY, t.data(), sizeof(double) * H.B, cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+int qg_apply_F(qg_handle *h, int transpose, const double *w, double *out, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  if (!transpose) H.cones.apply(w + H.NX, W.dpv, st);
+  StepArgs a{w, W.dpv, nullptr, out, nullptr, W.tY, W.tY2, nullptr, 0, W.part};
+  launch_step(H, M, transpose ? STEP_FT : STEP_F, a, st);
+  FinArgs f{H.B, PH_APPLY, transpose ? STEP_FT : STEP_F, nullptr, W.part, w, nullptr, out,
+            nullptr, nullptr, nullptr, nullptr};
+  launch_fin(H, M, f, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+int qg_jvp(qg_handle *h, const qg_perturbation *d, const qg_lsmr_opts *opts, double *dx, double *dy, double *ds,
+           qg_diag *diag, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  PertDev pd{};
+  DevCsr tP, tA, tAT;
+  double *vP = nullptr, *vA = nullptr;
+  if (d->same_pattern) {
+    vP = dev_alloc<double>(H.P.nnz);
+    vA = dev_alloc<double>(H.A.nnz);
+    launch_gather(H.P.perm, d->dP_vals, vP, H.P.nnz, st);
+    launch_gather(H.A.perm, d->dA_vals, vA, H.A.nnz, st);
+    pd.dP_rp = H.P.rp; pd.dP_col = H.P.col; pd.dP_val = vP;
+    pd.dA_rp = H.A.rp; pd.dA_col = H.A.col; pd.dA_val = vA;
+    pd.dAT_rp = H.AT.rp; pd.dAT_col = H.AT.col; pd.dAT_val = d->dA_vals;
+  } else {
+    std::vector<int64_t> pn(d->dP_nnz, d->dP_nnz + H.B), an(d->dA_nnz, d->dA_nnz + H.B);
+    CscBatch cp{d->dP_colptr, d->dP_rowidx, d->dP_vals, H.n, H.n, pn};
+    csc_to_csr(cp, tP, nullptr, false, st);
+    CscBatch ca{d->dA_colptr, d->dA_rowidx, d->dA_vals, H.n, H.m, an};
+    csc_to_csr(ca, tA, &tAT, false, st);
+    pd.dP_rp = tP.rp; pd.dP_col = tP.col; pd.dP_val = tP.val;
+    pd.dA_rp = tA.rp; pd.dA_col = tA.col; pd.dA_val = tA.val;
+    pd.dAT_rp = tAT.rp; pd.dAT_col = tAT.col; pd.dAT_val = d->dA_vals;
+  }
+  pd.dq = d->dq;
+  pd.db = d->db;
+  try {
+    long long cap;
+    lsmr_begin(H, *opts, st, cap);
+    launch_jvp_rhs(H, M, pd, W.u, W.part, st);
+    lsmr_solve(H, M, true, RHS_JVP, cap, st);
+    lsmr_finish(H, diag, st);
+    // D phi: dy/ds need D Pi(dz_mid)
+    H.cones.apply(W.x + H.NX, W.tY, st);
+    launch_dphi(H, M, W.x, W.tY, dx, dy, ds, st);
+    QG_CUDA(cudaStreamSynchronize(st));
+  } catch (...) {
+    dev_free(vP); dev_free(vA); tP.release(); tA.release(); tAT.release();
+    throw;
+  }
+  dev_free(vP); dev_free(vA); tP.release(); tA.release(); tAT.release();
+  QG_API_END
+}
+
+int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds, const qg_lsmr_opts *opts,
+           double *dP_vals, double *dA_vals, double *dq, double *db, qg_diag *diag, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  long long cap;
+  lsmr_begin(H, *opts, st, cap);
+  // dz = D phi'(delta): D Pi(dy + ds) - ds ; rhs = -dz ; D Pi(rhs_Y) for the first F
+  launch_add(H, dy, ds, W.tY2, H.NY, st);
+  H.cones.apply(W.tY2, W.tY, st);
+  launch_vjp_rhs(H, M, dx, dy, ds, W.tY, W.u, W.part, st);
+  H.cones.apply(W.u + H.NX, W.dpu, st);
+  lsmr_solve(H, M, false, RHS_VJP, cap, st);
+  lsmr_finish(H, diag, st);
+  launch_vjp_grad(H, M, W.x, dP_vals, dA_vals, dq, db, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+int qg_check(qg_handle *h, const double *x, const double *y, const double *s, double *report, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  // projections of s onto K and y onto K* (cones.py:926-941); the prepared
+  // derivative at the embedding point is left untouched
+  H.cones.prepare(s, W.tY, 0, false, st);
+  H.cones.check_errors(st);
+  H.cones.prepare(y, W.tY2, 1, false, st);
+  H.cones.check_errors(st);
+  double *rep = dev_alloc<double>(5 * (size_t)H.B);
+  launch_kkt(H, M, x, y, s, W.tY, W.tY2, W.part, rep, st);
+  QG_CUDA(cudaMemcpyAsync(report, rep, sizeof(double) * 5 * H.B, cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  dev_free(rep);
+  QG_API_END
+}
+
+int qg_spmv_csc(int64_t nrows, int64_t ncols, const int64_t *col_ptr, const int64_t *row_idx, const double *values,
+                int64_t nnz, int adjoint, const double *x, double *out, void *stream) {
+  QG_API_BEGIN
+  cudaStream_t st = (cudaStream_t)stream;
+  DevCsr t, tc;
+  CscBatch c{col_ptr, row_idx, values, {ncols}, {nrows}, {nnz}};
+  csc_to_csr(c, t, &tc, false, st);
+  if (adjoint) {
+    tc.val = dev_alloc<double>(nnz);
+    if (nnz) QG_CUDA(cudaMemcpyAsync(tc.val, values, sizeof(double) * nnz, cudaMemcpyDeviceToDevice, st));
+    launch_csr_spmv(tc.rp, tc.col, tc.val, ncols, x, out, st);
+  } else {
+    launch_csr_spmv(t.rp, t.col, t.val, nrows, x, out, st);
+  }
+  QG_CUDA(cudaStreamSynchronize(st));
+  t.release();
+  tc.release();
+  QG_API_END
+}
+
+// ----------------------------------------------------- cone calculus ----
+struct ConesHandle {
+  ConeTable t;
+};
+
+int qg_cones_create(qg_cones **out, const qg_cone_block *blocks, int64_t nblocks, void *stream) {
+  QG_API_BEGIN
+  auto *c = new ConesHandle();
+  try {
+    std::vector<std::vector<qg_cone_block>> per(1);
+    per[0].assign(blocks, blocks + nblocks);
+    int64_t m = 0;
+    for (auto &b : per[0]) m += b.dim;
+    std::vector<int64_t> yoff{0, m};
+    c->t.build(per, yoff, 1024, (cudaStream_t)stream);
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  *out = reinterpret_cast<qg_cones *>(c);
+  QG_API_END
+}
+
+int qg_cones_destroy(qg_cones *c) {
+  QG_API_BEGIN
+  delete reinterpret_cast<ConesHandle *>(c);
+  QG_API_END
+}
+
+int qg_cones_project(qg_cones *c, int dual, const double *z, double *out, void *stream) {
+  QG_API_BEGIN
+  ConeTable &t = reinterpret_cast<ConesHandle *>(c)->t;
+  cudaStream_t st = (cudaStream_t)stream;
+  t.prepare(z, out, dual, false, st);
+  t.check_errors(st);
+  QG_API_END
+}
+
+int qg_cones_prepare(qg_cones *c, int dual, const double *z, void *stream) {
+  QG_API_BEGIN
+  ConeTable &t = reinterpret_cast<ConesHandle *>(c)->t;
+  cudaStream_t st = (cudaStream_t)stream;
+  t.prepare(z, nullptr, dual, true, st);
+  t.check_errors(st);
+  QG_API_END
+}
+
+int qg_cones_apply(qg_cones *c, const double *dz, double *out, void *stream) {
+  QG_API_BEGIN
+  ConeTable &t = reinterpret_cast<ConesHandle *>(c)->t;
+  cudaStream_t st = (cudaStream_t)stream;
+  t.apply(dz, out, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+}  // extern "C"

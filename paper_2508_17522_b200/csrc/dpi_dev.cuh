@@ -1,0 +1,211 @@
+// Blockwise projection-derivative application for one work unit (CTA-wide),
+// and the CTA-level PSD Jacobi eigensolver used by the preparation kernels.
+//
+// Reference semantics: ConeDerivative.matvec (cones.py:886-906) with the
+// per-kind appliers of cones.py:740-795, 837-883; svec layout cones.py:176-202.
+#pragma once
+
+#include "cones_dev.cuh"
+#include "qg_common.cuh"
+
+namespace qg {
+
+constexpr int kMaxPsdOrder = 64;
+constexpr double kSqrt2 = 1.4142135623730951;
+
+__device__ __forceinline__ int svec_index(int i, int j, int d) {  // i >= j
+  return j * d - (j * (j - 1)) / 2 + (i - j);
+}
+
+// Elementwise (zero / nonneg) derivative weight (cones.py:837-848, 867-872).
+__device__ __forceinline__ double elem_weight(int kind, int dual, double z) {
+  if (kind == QG_CONE_ZERO) return dual ? 1.0 : 0.0;
+  return z > 0.0 ? 1.0 : (z == 0.0 ? 0.5 : 0.0);
+}
+
+// SOC applier (cones.py:740-764) executed by one warp for one block.
+__device__ __forceinline__ void soc_apply_warp(const double *zb, int dim, double nu, int code,
+                                               const double *in, double *out) {
+  const int lane = threadIdx.x & 31;
+  if (code != 3) {
+    const double f = (code == 0) ? 0.0 : (code == 1 ? 1.0 : 0.5);
+    for (int i = lane; i < dim; i += 32) out[i] = (code == 0) ? 0.0 : (code == 1 ? in[i] : f * in[i]);
+    return;
+  }
+  const double t = zb[0], dt = in[0];
+  double part = 0.0;
+  for (int i = 1 + lane; i < dim; i += 32) part += zb[i] * in[i];
+  const double udu = warp_sum(part);
+  const double two_nu = 2.0 * nu;
+  const double c = (t / (nu * nu)) * udu;
+  const double tn = t + nu;
+  for (int i = lane; i < dim; i += 32) {
+    double v;
+    if (i == 0) v = nu * dt + udu;
+    else v = (zb[i] * dt + tn * in[i]) - c * zb[i];
+    out[i] = v / two_nu;
+  }
+}
+
+// PSD applier (cones.py:791-793): out = svec(V (B o (V' smat(in) V)) V').
+// CTA-wide; smem holds 4 order^2 doubles.  V, B column-major in global.
+static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
+                              double *sm) {
+  double *V = sm, *S = sm + d * d, *T = sm + 2 * d * d, *W = sm + 3 * d * d;
+  const int dd = d * d;
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+    V[idx] = Vg[idx];
+    const int i = idx % d, j = idx / d;  // S column major: S[i + j d]
+    const int a = i >= j ? i : j, b = i >= j ? j : i;
+    const double v = in[svec_index(a, b, d)];
+    S[idx] = (a == b) ? v : v / kSqrt2;
+  }
+  __syncthreads();
+  // T = V' S   (T[i,j] = sum_k V[k,i] S[k,j])
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+    const int i = idx % d, j = idx / d;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += V[k + i * d] * S[k + j * d];
+    T[idx] = s;
+  }
+  __syncthreads();
+  // W = (T V) o B
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+    const int i = idx % d, j = idx / d;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += T[i + k * d] * V[k + j * d];
+    W[idx] = Bg[idx] * s;
+  }
+  __syncthreads();
+  // T = V W
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+    const int i = idx % d, j = idx / d;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += V[i + k * d] * W[k + j * d];
+    T[idx] = s;
+  }
+  __syncthreads();
+  // out = svec(T V')
+  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
+    const int i = idx % d, j = idx / d;
+    if (i < j) continue;
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) s += T[i + k * d] * V[j + k * d];
+    out[svec_index(i, j, d)] = (i == j) ? s : s * kSqrt2;
+  }
+  __syncthreads();
+}
+
+// Apply D Pi to the unit's rows.  in/out are indexed by (row - unit.row0);
+// they may live in global memory (written by this CTA before a barrier).
+static __device__ void dpi_apply_unit(const DpiView &dv, const Unit &u, const double *in, double *out, double *sm) {
+  if (u.cls == CLS_ELEM) {
+    const BlockInfo b = dv.blk[u.blk0];
+    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+      const int o = r - u.row0;
+      out[o] = elem_weight(b.kind, dv.dual, dv.zmid[r]) * in[o];
+    }
+  } else if (u.cls == CLS_SOC) {
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int k = u.blk0 + warp; k < u.blk1; k += nw) {
+      const BlockInfo b = dv.blk[k];
+      const int o = b.row - u.row0;
+      soc_apply_warp(dv.zmid + b.row, b.dim, dv.soc_nu[b.param], dv.soc_code[b.param], in + o, out + o);
+    }
+  } else if (u.cls == CLS_PSD) {
+    const BlockInfo b = dv.blk[u.blk0];
+    const double *V = dv.psd + b.param;
+    const int d = b.order;
+    psd_apply_cta(V, V + d * d, d, in + (b.row - u.row0), out + (b.row - u.row0), sm);
+  } else {  // CLS_TRI
+    for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+      const BlockInfo b = dv.blk[k];
+      const int o = b.row - u.row0;
+      const double *D = dv.tri_D + 9 * b.param;
+      double Dl[9], dd[3] = {in[o], in[o + 1], in[o + 2]}, oo[3];
+#pragma unroll
+      for (int i = 0; i < 9; ++i) Dl[i] = D[i];
+      tri_apply(Dl, dv.tri_flip[b.param], dd, oo);
+      out[o] = oo[0]; out[o + 1] = oo[1]; out[o + 2] = oo[2];
+    }
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------ PSD Jacobi (CTA-wide) --
+// Symmetric A (column major, d x d, in smem) -> eigenvalues lam[d] and
+// eigenvectors V (columns) by parallel cyclic Jacobi with round-robin pair
+// ordering.  Scratch: rot[2*32] doubles + pairs.
+static __device__ void jacobi_eigh_cta(double *A, double *V, double *lam, int d, double *rot, int *flag) {
+  const int dp = d + (d & 1);          // players (one dummy when d is odd)
+  const int npair = dp / 2;
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) V[idx] = (idx % d == idx / d) ? 1.0 : 0.0;
+  __shared__ double s_fro;
+  if (threadIdx.x == 0) {
+    double f = 0.0;
+    for (int k = 0; k < d * d; ++k) f += A[k] * A[k];
+    s_fro = sqrt(f);
+  }
+  __syncthreads();
+  const double floor_abs = 1e-18 * s_fro;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int round = 0; round < dp - 1; ++round) {
+      // rotation parameters, one thread per pair
+      if ((int)threadIdx.x < npair) {
+        const int k = threadIdx.x;
+        auto player = [&](int pos) { return pos == 0 ? 0 : 1 + ((pos - 1 + round) % (dp - 1)); };
+        int p = player(k), q = player(dp - 1 - k);
+        if (p > q) { int t = p; p = q; q = t; }
+        double c = 1.0, s = 0.0;
+        if (q < d) {
+          const double apq = A[p + q * d], app = A[p + p * d], aqq = A[q + q * d];
+          const double thr = 2.220446049250313e-16 * sqrt(fabs(app * aqq));
+          if (fabs(apq) > floor_abs && fabs(apq) > thr) {
+            const double th = (aqq - app) / (2.0 * apq);
+            const double t = (th >= 0.0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+            *flag = 1;
+          }
+        }
+        rot[4 * k + 0] = c; rot[4 * k + 1] = s;
+        rot[4 * k + 2] = (double)p; rot[4 * k + 3] = (double)q;
+      }
+      __syncthreads();
+      // rows: A <- J' A
+      for (int idx = threadIdx.x; idx < npair * d; idx += blockDim.x) {
+        const int k = idx / d, col = idx % d;
+        const double c = rot[4 * k], s = rot[4 * k + 1];
+        const int p = (int)rot[4 * k + 2], q = (int)rot[4 * k + 3];
+        if (q >= d || s == 0.0) continue;
+        const double ap = A[p + col * d], aq = A[q + col * d];
+        A[p + col * d] = c * ap - s * aq;
+        A[q + col * d] = s * ap + c * aq;
+      }
+      __syncthreads();
+      // columns: A <- A J ; V <- V J
+      for (int idx = threadIdx.x; idx < npair * d; idx += blockDim.x) {
+        const int k = idx / d, row = idx % d;
+        const double c = rot[4 * k], s = rot[4 * k + 1];
+        const int p = (int)rot[4 * k + 2], q = (int)rot[4 * k + 3];
+        if (q >= d || s == 0.0) continue;
+        const double ap = A[row + p * d], aq = A[row + q * d];
+        A[row + p * d] = c * ap - s * aq;
+        A[row + q * d] = s * ap + c * aq;
+        const double vp = V[row + p * d], vq = V[row + q * d];
+        V[row + p * d] = c * vp - s * vq;
+        V[row + q * d] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+    const int any = *flag;
+    __syncthreads();
+    if (!any) break;
+  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) lam[i] = A[i + i * d];
+  __syncthreads();
+}
+
+}  // namespace qg

@@ -1,0 +1,93 @@
+// The prepared batch ("QCP object" of the north star): problem data in CSR
+// form, the projected embedding point, the prepared D Pi, work units and the
+// LSMR workspace.  All device-resident; immutable after qg_create_batch
+// except for the per-call workspace.
+#pragma once
+
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "cone_table.h"
+#include "qg_common.cuh"
+
+namespace qg {
+
+// Per-problem embedding constants (embedding.py:337-344, 399-417).
+struct Embed {
+  double tau;   // (Pi z)_N = max(z_N, 0)
+  double zN;    // z_N (= 1 from embed)
+  double last;  // D Pi on the last coordinate: 1 if z_N > 0 else 0
+  double xPx;   // xbar' P xbar
+};
+
+// Per-problem LSMR state (lsmr.py:57-184), resident in HBM.
+struct Lsmr {
+  double alpha, beta, s_u, s_v, normb;
+  double zetabar, alphabar, rho, rhobar, cbar, sbar;
+  double betadd, betad, rhodold, tautildeold, thetatilde, zeta, d, normA2;
+  double normr, normar, normA, normx;
+  double c_hbar, c_x, c_h;
+  double s_in, c_out;     // coefficients of the next half step
+  double atol, btol;
+  long long itn, max_iter;
+  int active, converged, skip_v, status;
+};
+
+// Transposed / reinterpreted sparse structure on the device.
+struct DevCsr {
+  int32_t *rp = nullptr;   // row pointer (global rows)
+  int32_t *col = nullptr;  // global column index
+  double *val = nullptr;
+  int32_t *perm = nullptr; // CSR position -> global CSC entry (transposes)
+  int64_t nrows = 0, nnz = 0;
+  void release();
+};
+
+struct Workspace {
+  double *u = nullptr, *v = nullptr, *h = nullptr, *hb = nullptr, *x = nullptr;  // EVec
+  double *dpu = nullptr, *dpv = nullptr, *tY = nullptr, *tY2 = nullptr;          // Y
+  double *part = nullptr;
+  Lsmr *st = nullptr;
+  int *d_nactive = nullptr;
+  int *h_nactive = nullptr;  // pinned
+  void release();
+};
+
+struct Handle {
+  int B = 0;
+  std::vector<int64_t> n, m, xoff, yoff, nnzP, nnzA, noffP, noffA;
+  int64_t NX = 0, NY = 0, NE = 0;  // NE = NX + NY + B
+  DevCsr P;    // CSR of P (exact transpose of the CSC input)
+  DevCsr Pc;   // CSC structure of P read as rows = columns (for dP emission)
+  DevCsr A;    // CSR of A
+  DevCsr AT;   // CSC of A read as CSR of A' (rows = columns of A, cols = global Y)
+  ConeTable cones;
+  std::vector<Unit> xunits;
+  std::vector<int64_t> xunit_ptr;
+  Unit *d_xunits = nullptr;
+  int gx = 1, gy = 1;            // SpMV group sizes (X rows / Y rows)
+  int64_t *d_xoff = nullptr, *d_yoff = nullptr;
+  int64_t *d_xunit_ptr = nullptr, *d_yunit_ptr = nullptr;
+  double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;
+  double *Pxbar = nullptr;
+  Embed *emb = nullptr;
+  Workspace ws;
+  std::mutex mu;  // one jvp/vjp at a time per handle (workspace reuse)
+
+  int nxu() const { return (int)xunits.size(); }
+  int nyu() const { return (int)cones.units.size(); }
+  ~Handle();
+};
+
+// CSC (int64, concatenated per problem) -> device CSR (int32) by a stable
+// radix sort on global row keys.  Also returns the CSC structure itself in
+// CSR-of-transpose form when `csc_as_rows` is non-null.
+struct CscBatch {
+  const int64_t *colptr, *rowidx;
+  const double *vals;
+  std::vector<int64_t> ncols, nrows, nnz;  // per problem
+};
+void csc_to_csr(const CscBatch &in, DevCsr &out, DevCsr *csc_as_rows, bool keep_perm, cudaStream_t st);
+
+}  // namespace qg

@@ -1,0 +1,464 @@
+// The hot path: one LSMR iteration on the implicit-function operator
+//   F w  = ((D_uQ - I) D Pi + I) w / z_N        (embedding.py:399-427)
+// and its transpose, for a whole batch of problems at once.
+//
+// Per iteration:
+//   k_step<F>   u <- s_in * F v  - c_out * u   fused CSR SpMV (P, A', A) + epilogue
+//   k_fin       per problem: T component, ||u||, scalars          (lsmr.py:115-118)
+//   k_step<FT>  v <- s_in * F' u - c_out * v   SpMV + D Pi epilogue (x2) per cone block
+//   k_fin       ||v||, Givens recurrences, update coefficients   (lsmr.py:119-171)
+//   k_update    hbar, x, h axpys + ||x||^2 partials               (lsmr.py:142-144, 168)
+//   k_fin       stopping rules                                     (lsmr.py:173-182)
+// The LSMR vectors are kept unnormalised ("raw") with per-problem scale
+// factors, so no kernel has to wait for a norm before writing its output.
+#include "dpi_dev.cuh"
+#include "ops_dev.cuh"
+#include "operator.h"
+
+namespace qg {
+
+__device__ __forceinline__ bool lsmr_runs(const Lsmr *st, int p, int is_v_step, double &s_in, double &c_out) {
+  if (!st) { s_in = 1.0; c_out = 0.0; return true; }
+  const Lsmr &L = st[p];
+  s_in = L.s_in;
+  c_out = L.c_out;
+  return L.active && !(is_v_step && L.skip_v);
+}
+
+// ------------------------------------------------------------- op steps --
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
+  extern __shared__ double sm[];
+  __shared__ double red[kWarps * kSlots];
+  const bool isx = (int)blockIdx.x < M.nxu;
+  const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
+  const int p = u.prob;
+  double s_in, c_out;
+  if (!lsmr_runs(a.st, p, a.is_v_step, s_in, c_out)) return;  // CTA-uniform
+  const Embed E = M.emb[p];
+  const double *inX = a.in, *inY = a.in + M.NX;
+  const double wN = a.in[M.NX + M.NY + p];
+  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (isx) {
+    const int G = M.gx, lg = lane & (G - 1), gpw = 32 / G;
+    for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
+      const int r = base + lane / G;
+      const bool valid = r < u.row1;
+      double s1 = 0.0, s2 = 0.0;
+      if (valid) {
+        s1 = row_dot(M.P_rp, M.P_col, M.P_val, inX, r, lg, G);
+        s2 = row_dot(M.AT_rp, M.AT_col, M.AT_val, KIND == STEP_F ? a.dpin : inY, r, lg, G);
+      }
+      s1 = gsum(s1, G);
+      s2 = gsum(s2, G);
+      if (valid && lg == 0) {
+        const double w = inX[r];
+        double res;
+        if (KIND == STEP_F) {
+          // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
+          const double o1 = (s1 + s2) + wN * M.q[r];
+          res = ((o1 - w) + w) / E.zN;
+          acc[0] += M.Pxbar[r] * w;
+        } else {
+          // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
+          const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
+          res = ((g - w) + w) / E.zN;
+        }
+        acc[1] += M.q[r] * w;
+        const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
+        a.out[r] = o;
+        acc[2] += o * o;
+      }
+    }
+  } else {
+    double *outY = a.out + M.NX;
+    const double *oldY = a.old ? a.old + M.NX : nullptr;
+    const int G = M.gy, lg = lane & (G - 1), gpw = 32 / G;
+    if (KIND == STEP_F) {
+      for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
+        const int r = base + lane / G;
+        const bool valid = r < u.row1;
+        double s = valid ? row_dot(M.A_rp, M.A_col, M.A_val, inX, r, lg, G) : 0.0;
+        s = gsum(s, G);
+        if (valid && lg == 0) {
+          // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
+          const double o2 = (-s) + wN * M.b[r];
+          const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+          const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+          outY[r] = o;
+          acc[0] += M.b[r] * a.dpin[r];
+          acc[2] += o * o;
+        }
+      }
+    } else {
+      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
+      for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
+        const int r = base + lane / G;
+        const bool valid = r < u.row1;
+        double s = valid ? row_dot(M.A_rp, M.A_col, M.A_val, inX, r, lg, G) : 0.0;
+        s = gsum(s, G);
+        if (valid && lg == 0) a.tY[r] = (s - wN * M.b[r]) - inY[r];
+      }
+      __syncthreads();
+      // r = D Pi t  (blockwise, in the unit)
+      dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
+      // pass 2: (r + w2)/z_N, axpy, norms
+      for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+        const double w = inY[r];
+        const double res = (a.tY2[r] + w) / E.zN;
+        const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+        outY[r] = o;
+        acc[0] += M.b[r] * w;
+        acc[2] += o * o;
+      }
+      __syncthreads();
+      if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
+    }
+  }
+  double tot[kSlots];
+  cta_sum_slots(acc, red, tot);
+  if (threadIdx.x == 0 && a.part)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
+}
+
+// -------------------------------------------------------------- update --
+// hbar = h - c1 hbar ; x = x + c2 hbar ; h = v s_v - c3 h   (lsmr.py:142-144)
+__global__ void __launch_bounds__(kThreads) k_update(Mats M, UpdArgs a) {
+  __shared__ double red[kWarps * kSlots];
+  const bool isx = (int)blockIdx.x < M.nxu;
+  const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
+  const Lsmr &L = a.st[u.prob];
+  if (!L.active) return;
+  const double c1 = L.c_hbar, c2 = L.c_x, c3 = L.c_h, sv = L.s_v;
+  const int64_t off = isx ? 0 : M.NX;
+  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t r = off + u.row0 + threadIdx.x; r < off + u.row1; r += blockDim.x) {
+    const double hb = a.h[r] - c1 * a.hb[r];
+    const double x = a.x[r] + c2 * hb;
+    a.h[r] = a.v[r] * sv - c3 * a.h[r];
+    a.hb[r] = hb;
+    a.x[r] = x;
+    acc[0] += x * x;
+  }
+  double tot[kSlots];
+  cta_sum_slots(acc, red, tot);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
+}
+
+// ----------------------------------------------------------- finalize --
+__device__ __forceinline__ double dsign(double v) { return (v > 0.0) ? 1.0 : ((v < 0.0) ? -1.0 : 0.0); }
+
+__device__ __forceinline__ void sym_ortho(double a, double b, double &c, double &s, double &r) {   // lsmr.py:38-54
+  if (b == 0.0) { c = dsign(a); s = 0.0; r = fabs(a); return; }
+  if (a == 0.0) { c = 0.0; s = dsign(b); r = fabs(b); return; }
+  if (fabs(b) > fabs(a)) {
+    const double t = a / b;
+    s = dsign(b) / sqrt(1.0 + t * t);
+    c = s * t;
+    r = b / s;
+  } else {
+    const double t = b / a;
+    c = dsign(a) / sqrt(1.0 + t * t);
+    s = c * t;
+    r = a / c;
+  }
+}
+
+// T component of an operator step output (embedding.py:232-237, 261 and 420-425).
+__device__ __forceinline__ double t_component(int kind, const Embed &E, double wN, const double sx[kSlots],
+                                              const double sy[kSlots]) {
+  if (kind == STEP_F) {
+    const double outN = ((-(2.0 / E.tau)) * sx[0] - sx[1] - sy[0]) + (E.xPx / (E.tau * E.tau)) * wN;
+    return ((outN - E.last * wN) + wN) / E.zN;
+  }
+  const double gN = (sx[1] + sy[0]) + (E.xPx / (E.tau * E.tau)) * wN;
+  return (E.last * (gN - wN) + wN) / E.zN;
+}
+
+__global__ void k_fin(Mats M, FinArgs a) {
+  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= a.B) return;
+  Lsmr *L = a.st ? a.st + p : nullptr;
+  if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
+  if (L && a.phase == PH_STEP_V && L->skip_v) {
+    // fall through: v-step did not run, only the recurrences do
+  }
+  // deterministic per-problem sums of the unit partials
+  double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
+  for (int64_t k = M.xu_ptr[p] + lane; k < M.xu_ptr[p + 1]; k += 32)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) sx[j] += a.part[k * kSlots + j];
+  for (int64_t k = M.yu_ptr[p] + lane; k < M.yu_ptr[p + 1]; k += 32)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) sy[j] += a.part[(M.nxu + k) * kSlots + j];
+#pragma unroll
+  for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
+  if (lane != 0) return;
+  const Embed E = M.emb[p];
+  const int64_t T = M.NX + M.NY + p;
+
+  if (a.phase == PH_APPLY) {
+    a.out[T] = t_component(a.kind, E, a.in[T], sx, sy);
+    return;
+  }
+  if (a.phase == PH_RHS) {
+    // rhs_N from the assembly partials; then lsmr.py:72-80
+    double rN;
+    if (a.kind == RHS_JVP) {
+      const double outN = ((-sx[0]) / E.tau - sx[1]) - sy[0];   // embedding.py:291
+      rN = (-outN) / fabs(E.zN);
+    } else {
+      const double dzN = ((-sx[0]) - sy[0]) - sy[1];             // solution_map.py:259
+      rN = -dzN;
+    }
+    a.out[T] = rN;
+    const double beta = sqrt((sx[2] + sy[2]) + rN * rN);
+    L->beta = beta;
+    L->normb = beta;
+    L->itn = 0;
+    L->status = 0;
+    L->skip_v = 0;
+    L->alpha = 0.0;
+    L->s_v = 1.0;
+    if (beta > 0.0) {
+      L->s_u = 1.0 / beta;
+      L->s_in = L->s_u;
+      L->c_out = 0.0;
+      L->active = 1;
+    } else {
+      L->s_u = 1.0;
+      L->active = 0;
+      L->converged = 1;
+      L->normr = beta;
+      L->normar = 0.0;
+    }
+    return;
+  }
+  if (a.phase == PH_INIT_V) {
+    const double vN = t_component(a.kind, E, a.in[T], sx, sy) * L->s_in;
+    a.out[T] = vN;
+    const double alpha = sqrt((sx[2] + sy[2]) + vN * vN);
+    L->alpha = alpha;
+    L->s_v = alpha > 0.0 ? 1.0 / alpha : 1.0;
+    const double beta = L->beta;
+    if (alpha * beta == 0.0) {
+      L->active = 0;
+      L->converged = 1;
+      L->normr = beta;
+      L->normar = 0.0;
+      return;
+    }
+    L->zetabar = alpha * beta;
+    L->alphabar = alpha;
+    L->rho = L->rhobar = L->cbar = 1.0;
+    L->sbar = 0.0;
+    L->betadd = beta;
+    L->betad = 0.0;
+    L->rhodold = 1.0;
+    L->tautildeold = L->thetatilde = L->zeta = L->d = 0.0;
+    L->normA2 = alpha * alpha;
+    L->normr = beta;
+    L->normar = alpha * beta;
+    L->c_hbar = L->c_x = L->c_h = 0.0;
+    a.h[T] = vN * L->s_v;
+    a.hb[T] = 0.0;
+    a.x[T] = 0.0;
+    L->s_in = L->s_v;
+    L->c_out = alpha * L->s_u;
+    if (L->max_iter <= 0) { L->active = 0; L->converged = 0; }
+    return;
+  }
+  if (a.phase == PH_STEP_U) {
+    L->itn += 1;
+    const double uN = L->s_in * t_component(a.kind, E, a.in[T], sx, sy) - L->c_out * a.old[T];
+    a.out[T] = uN;
+    const double beta = sqrt((sx[2] + sy[2]) + uN * uN);
+    L->beta = beta;
+    if (beta > 0.0) {
+      L->s_u = 1.0 / beta;
+      L->skip_v = 0;
+      L->s_in = L->s_u;
+      L->c_out = beta * L->s_v;
+    } else {
+      L->s_u = 1.0;
+      L->skip_v = 1;
+    }
+    return;
+  }
+  if (a.phase == PH_STEP_V) {
+    double alpha = L->alpha;
+    if (!L->skip_v) {
+      const double vN = L->s_in * t_component(a.kind, E, a.in[T], sx, sy) - L->c_out * a.old[T];
+      a.out[T] = vN;
+      alpha = sqrt((sx[2] + sy[2]) + vN * vN);
+      L->alpha = alpha;
+      L->s_v = alpha > 0.0 ? 1.0 / alpha : 1.0;
+    }
+    const double beta = L->beta;
+    if (!(isfinite(alpha) && isfinite(beta))) {
+      L->status = QG_ERR_NUMERICAL;
+      L->active = 0;
+      return;
+    }
+    // lsmr.py:127-171
+    double chat, shat, alphahat;
+    sym_ortho(L->alphabar, 0.0, chat, shat, alphahat);
+    const double rhoold = L->rho;
+    double c, s, rho;
+    sym_ortho(alphahat, beta, c, s, rho);
+    const double thetanew = s * alpha;
+    L->alphabar = c * alpha;
+    const double rhobarold = L->rhobar;
+    const double zetaold = L->zeta;
+    const double thetabar = L->sbar * rho;
+    const double rhotemp = L->cbar * rho;
+    double cbar, sbar, rhobar;
+    sym_ortho(rhotemp, thetanew, cbar, sbar, rhobar);
+    const double zeta = cbar * L->zetabar;
+    L->zetabar = -sbar * L->zetabar;
+    L->c_hbar = thetabar * rho / (rhoold * rhobarold);
+    L->c_x = zeta / (rho * rhobar);
+    L->c_h = thetanew / rho;
+    const double betaacute = chat * L->betadd;
+    const double betacheck = -shat * L->betadd;
+    const double betahat = c * betaacute;
+    L->betadd = -s * betaacute;
+    const double thetatildeold = L->thetatilde;
+    double ctildeold, stildeold, rhotildeold;
+    sym_ortho(L->rhodold, thetabar, ctildeold, stildeold, rhotildeold);
+    L->thetatilde = stildeold * rhobar;
+    L->rhodold = ctildeold * rhobar;
+    L->betad = -stildeold * L->betad + ctildeold * betahat;
+    L->tautildeold = (zetaold - thetatildeold * L->tautildeold) / rhotildeold;
+    const double taud = (zeta - L->thetatilde * L->tautildeold) / L->rhodold;
+    L->d = L->d + betacheck * betacheck;
+    const double bt = L->betad - taud;
+    L->normr = sqrt(L->d + bt * bt + L->betadd * L->betadd);
+    L->normA2 = L->normA2 + beta * beta;
+    L->normA = sqrt(L->normA2);
+    L->normA2 = L->normA2 + alpha * alpha;
+    L->normar = fabs(L->zetabar);
+    L->rho = rho;
+    L->rhobar = rhobar;
+    L->cbar = cbar;
+    L->sbar = sbar;
+    L->zeta = zeta;
+    // T parts of the vector updates
+    const double hb = a.h[T] - L->c_hbar * a.hb[T];
+    a.x[T] = a.x[T] + L->c_x * hb;
+    a.h[T] = a.v[T] * L->s_v - L->c_h * a.h[T];
+    a.hb[T] = hb;
+    L->s_in = L->s_v;
+    L->c_out = alpha * L->s_u;
+    return;
+  }
+  if (a.phase == PH_STEP_X) {   // lsmr.py:168-184
+    const double xN = a.x[T];
+    const double normx = sqrt((sx[0] + sy[0]) + xN * xN);
+    L->normx = normx;
+    const double normr = L->normr, normar = L->normar, normA = L->normA, normb = L->normb;
+    if (!(isfinite(normr) && isfinite(normar) && isfinite(normx))) {
+      L->status = QG_ERR_NUMERICAL;
+      L->active = 0;
+      return;
+    }
+    bool stop = false;
+    if (normar == 0.0) stop = true;
+    else {
+      const double test1 = normr / normb;
+      const double test2 = normr > 0.0 ? normar / (normA * normr) : 0.0;
+      const double rtol = L->btol + L->atol * normA * normx / normb;
+      const double t1 = test1 / (1.0 + normA * normx / normb);
+      if (1.0 + test2 <= 1.0 || 1.0 + t1 <= 1.0) stop = true;
+      else if (test2 <= L->atol || test1 <= rtol) stop = true;
+    }
+    if (stop) { L->active = 0; L->converged = 1; }
+    else if (L->itn >= L->max_iter) { L->active = 0; L->converged = 0; }
+  }
+}
+
+__global__ void k_count_active(const Lsmr *st, int B, int *out) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int p = threadIdx.x; p < B; p += blockDim.x) c += st[p].active ? 1 : 0;
+  atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) *out = cnt;
+}
+
+__global__ void k_init_state(Lsmr *st, int B, double atol, double btol, const long long *max_iter) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= B) return;
+  Lsmr L{};
+  L.atol = atol;
+  L.btol = btol;
+  L.max_iter = max_iter[p];
+  L.s_u = L.s_v = 1.0;
+  st[p] = L;
+}
+
+// ---------------------------------------------------------------- host --
+Mats make_mats(const Handle &H) {
+  Mats M{};
+  M.P_rp = H.P.rp; M.P_col = H.P.col; M.P_val = H.P.val;
+  M.AT_rp = H.AT.rp; M.AT_col = H.AT.col; M.AT_val = H.AT.val;
+  M.A_rp = H.A.rp; M.A_col = H.A.col; M.A_val = H.A.val;
+  M.xu = H.d_xunits; M.yu = H.cones.d_units;
+  M.nxu = H.nxu(); M.nyu = H.nyu();
+  M.xu_ptr = H.d_xunit_ptr; M.yu_ptr = H.d_yunit_ptr;
+  M.q = H.q; M.b = H.b; M.Pxbar = H.Pxbar; M.xbar = H.xbar; M.ybar = H.ybar; M.sbar = H.sbar;
+  M.emb = H.emb;
+  M.NX = H.NX; M.NY = H.NY;
+  M.gx = H.gx; M.gy = H.gy;
+  M.dpi = H.cones.view();
+  return M;
+}
+
+static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
+
+void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
+  const unsigned grid = (unsigned)(H.nxu() + H.nyu());
+  if (grid == 0) return;
+  const size_t smem = step_smem(H);
+  if (kind == STEP_F) {
+    k_step<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
+  } else {
+    if (smem > 48 * 1024)
+      QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_step<STEP_FT><<<grid, kThreads, smem, st>>>(M, a);
+  }
+  QG_LAUNCHED();
+}
+
+void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st) {
+  const unsigned grid = (unsigned)((H.B * 32 + 255) / 256);
+  k_fin<<<grid, 256, 0, st>>>(M, a);
+  QG_LAUNCHED();
+}
+
+void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st) {
+  const unsigned grid = (unsigned)(H.nxu() + H.nyu());
+  if (grid == 0) return;
+  k_update<<<grid, kThreads, 0, st>>>(M, a);
+  QG_LAUNCHED();
+}
+
+void launch_count_active(const Handle &H, cudaStream_t st) {
+  k_count_active<<<1, 256, 0, st>>>(H.ws.st, H.B, H.ws.d_nactive);
+  QG_LAUNCHED();
+}
+
+void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st) {
+  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, d_max_iter);
+  QG_LAUNCHED();
+}
+
+}  // namespace qg

@@ -1,0 +1,77 @@
+// Host interface of the operator / LSMR / assembly kernels.
+#pragma once
+
+#include "handle.h"
+#include "ops_dev.cuh"
+
+namespace qg {
+
+enum StepKind { STEP_F = 0, STEP_FT = 1 };
+enum FinPhase { PH_APPLY = 0, PH_RHS = 1, PH_INIT_V = 2, PH_STEP_U = 3, PH_STEP_V = 4, PH_STEP_X = 5 };
+enum RhsKind { RHS_JVP = 0, RHS_VJP = 1 };
+
+struct StepArgs {
+  const double *in;    // EVec, raw
+  const double *dpin;  // Y: D Pi applied to in_Y (F step)
+  const double *old;   // EVec or null
+  double *out;         // EVec
+  double *dpout;       // Y: D Pi applied to out_Y (F' step), or null
+  double *tY, *tY2;    // Y scratch (F' step)
+  const Lsmr *st;      // per-problem coefficients / run flags; null = (1, 0), all run
+  int is_v_step;
+  double *part;
+};
+
+struct FinArgs {
+  int B;
+  int phase;
+  int kind;            // STEP_F / STEP_FT (or RhsKind for PH_RHS)
+  Lsmr *st;
+  const double *part;
+  const double *in;    // EVec (T component read)
+  const double *old;   // EVec
+  double *out;         // EVec (T component written)
+  double *h, *hb, *x, *v;
+};
+
+struct UpdArgs {
+  double *h, *hb, *x;
+  const double *v;
+  const Lsmr *st;
+  double *part;
+};
+
+Mats make_mats(const Handle &H);
+void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
+void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
+void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
+void launch_count_active(const Handle &H, cudaStream_t st);
+void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st);
+
+// assembly (assembly.cu)
+struct PertDev {
+  // dP as CSR over X rows (values in CSR order), dA as CSR over Y rows and as
+  // CSC-as-rows over X rows; dq, db.
+  const int32_t *dP_rp, *dP_col; const double *dP_val;
+  const int32_t *dA_rp, *dA_col; const double *dA_val;
+  const int32_t *dAT_rp, *dAT_col; const double *dAT_val;
+  const double *dq, *db;
+};
+void launch_jvp_rhs(const Handle &H, const Mats &M, const PertDev &d, double *u, double *part, cudaStream_t st);
+void launch_vjp_rhs(const Handle &H, const Mats &M, const double *dx, const double *dy, const double *ds,
+                    const double *dpi_dyds, double *u, double *part, cudaStream_t st);
+void launch_add(const Handle &H, const double *a, const double *b, double *out, int64_t n, cudaStream_t st);
+void launch_gather(const int32_t *perm, const double *src, double *dst, int64_t n, cudaStream_t st);
+void launch_dphi(const Handle &H, const Mats &M, const double *dz, const double *dpi_dz, double *dx, double *dy,
+                 double *ds, cudaStream_t st);
+void launch_vjp_grad(const Handle &H, const Mats &M, const double *w, double *dP, double *dA, double *dq,
+                     double *db, cudaStream_t st);
+void launch_embed_prep(const Handle &H, const double *x, const double *y, const double *s, double *zmid,
+                       cudaStream_t st);
+void launch_embed_consts(const Handle &H, const Mats &M, double *part, cudaStream_t st);
+void launch_csr_spmv(const int32_t *rp, const int32_t *col, const double *val, int64_t nrows, const double *x,
+                     double *out, cudaStream_t st);
+void launch_kkt(const Handle &H, const Mats &M, const double *x, const double *y, const double *s,
+                const double *projs, const double *projy, double *part, double *report_dev, cudaStream_t st);
+
+}  // namespace qg

@@ -1,0 +1,38 @@
+// Device-side argument bundles shared by the operator, LSMR and assembly
+// kernels.
+#pragma once
+
+#include "handle.h"
+
+namespace qg {
+
+struct Mats {
+  const int32_t *P_rp, *P_col; const double *P_val;
+  const int32_t *AT_rp, *AT_col; const double *AT_val;
+  const int32_t *A_rp, *A_col; const double *A_val;
+  const Unit *xu, *yu;
+  int nxu, nyu;
+  const int64_t *xu_ptr, *yu_ptr;  // [B+1] unit ranges per problem
+  const double *q, *b, *Pxbar, *xbar, *ybar, *sbar;
+  const Embed *emb;
+  int64_t NX, NY;
+  int gx, gy;
+  DpiView dpi;
+};
+
+// Group-of-G sum inside a warp (G power of two, runtime).
+__device__ __forceinline__ double gsum(double v, int G) {
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Row dot product by a group of G lanes: sum_k val[k] * vec[col[k]].
+__device__ __forceinline__ double row_dot(const int32_t *rp, const int32_t *col, const double *val,
+                                          const double *vec, int r, int lane_g, int G) {
+  double s = 0.0;
+  const int k1 = rp[r + 1];
+  for (int k = rp[r] + lane_g; k < k1; k += G) s += val[k] * vec[col[k]];
+  return s;
+}
+
+}  // namespace qg

@@ -1,0 +1,146 @@
+// Shared definitions of libqcpgrad (B200 / sm_100a).
+//
+// Layout of a prepared batch in HBM:
+//   embedding vectors: [X: sum n | Y: sum m | T: nprob]   fp64
+//   CSR(P)  over X rows, columns global X indices          int32 / fp64
+//   CSR(A)  over Y rows, columns global X indices          int32 / fp64
+//   CSR(A') over X rows, columns global Y indices          (= CSC(A))
+//   cone blocks: table + per-class work units; DPi parameters per block.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/qcpgrad.h"
+
+namespace qg {
+
+// ---------------------------------------------------------------- errors --
+struct Error {
+  int code;
+  std::string msg;
+};
+
+void set_error(int code, const std::string &msg);
+int fail(int code, const std::string &msg);
+void count_launch(int n = 1);
+
+#define QG_CUDA(expr)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      throw qg::Error{QG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+#define QG_LAUNCHED()                                                              \
+  do {                                                                             \
+    qg::count_launch();                                                            \
+    cudaError_t _e = cudaGetLastError();                                           \
+    if (_e != cudaSuccess)                                                         \
+      throw qg::Error{QG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)}; \
+  } while (0)
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kSlots = 4;  // partial-sum doubles per work unit
+
+// Block classes of the fused Y-side work units.
+enum UnitClass : int32_t { CLS_ELEM = 0, CLS_SOC = 1, CLS_PSD = 2, CLS_TRI = 3 };
+
+// Per-block parameter record (one per cone block of the batch).
+struct BlockInfo {
+  int32_t kind;     // qg_cone_kind
+  int32_t row;      // first global Y row
+  int32_t dim;
+  int32_t order;    // psd order
+  double alpha;     // pow exponent
+  int64_t param;    // soc index / tri index / psd storage offset (V then B)
+  int32_t prob;     // problem index
+  int32_t local;    // block index within its problem
+};
+
+// Prepared derivative data of the blockwise projection.
+//   elem (zero/nonneg):  weight derived from zmid on the fly
+//   soc:   soc_nu[blk], soc_code[blk] (0 zero map, 1 identity, 2 half, 3 formula)
+//   psd:   V (order^2, column major) and B (order^2) at BlockInfo::psd_off
+//   tri:   tri_D[9*blk] dense 3x3 and tri_flip[blk] (1 -> d - D d)
+struct DpiView {
+  const BlockInfo *blk;
+  const double *zmid;     // the point (Y layout)
+  const double *soc_nu;
+  const int32_t *soc_code;
+  const double *psd;
+  const double *tri_D;
+  const int32_t *tri_flip;
+  int32_t dual;           // derivative of the dual projection (else primal)
+};
+
+// A unit of work: a contiguous row range of one problem; Y-units also cover
+// whole cone blocks [blk0, blk1) of one class.
+struct Unit {
+  int32_t prob;
+  int32_t row0, row1;
+  int32_t blk0, blk1;
+  int32_t cls;
+};
+
+struct Csr {
+  int32_t nrows = 0;
+  int64_t nnz = 0;
+  int32_t *rowptr = nullptr;  // nrows+1 (global rows)
+  int32_t *col = nullptr;     // global column indices
+  double *val = nullptr;
+  int32_t *perm = nullptr;    // CSR position -> CSC entry (transposes only)
+};
+
+// ---------------------------------------------------------- device utils --
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+
+// Deterministic CTA reduction of kSlots values (fixed tree order); result in
+// out[] on thread 0.
+__device__ __forceinline__ void cta_sum_slots(double (&v)[kSlots], double *smem_red, double *out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) smem_red[warp * kSlots + k] = v[k];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) {
+      double s = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += smem_red[w * kSlots + k];
+      out[k] = s;
+    }
+  }
+  __syncthreads();
+}
+
+template <class T>
+inline T *dev_alloc(size_t count) {
+  if (count == 0) count = 1;
+  T *p = nullptr;
+  QG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  return p;
+}
+
+inline void dev_free(void *p) {
+  if (p) cudaFree(p);
+}
+
+}  // namespace qg

@@ -1,0 +1,432 @@
+"""Derivatives of the QCP solution map on the GPU -- the drop-in boundary.
+
+Mirrors the reference's public surface (solution_map.py:50-385): ``jvp`` /
+``vjp`` with the same keyword arguments, defaults, pre-check behaviour,
+return types and ``Diagnostics``.  Underneath, everything runs through the
+C ABI of libqcpgrad.so:
+
+* ``QCP`` -- the prepared "QCP object" of the north star: problem data and a
+  primal-dual solution uploaded once, the projection derivative prepared
+  once, then any number of ``jvp``/``vjp`` calls;
+* ``QCPBatch`` -- a batch of independent problems solved together (one
+  kernel sequence for the whole batch, per-problem LSMR scalars and stop
+  flags).
+
+Host arrays (NumPy) in, host arrays out, exactly like the reference; the
+``*_device`` methods take and return CUDA tensors for on-device pipelines.
+"""
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from paper_2508_17522_b200 import _native as N
+from paper_2508_17522_b200 import cones
+from paper_2508_17522_b200.embedding import DataPerturbation, ProblemData
+from paper_2508_17522_b200.errors import DomainError, ValidationError
+from paper_2508_17522_b200.sparse import CscMatrix, same_pattern
+
+
+def _vector(name, v, length=None):
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    if v.ndim != 1 or (length is not None and v.shape != (length,)):
+        raise ValidationError(f"{name} must be a vector of length {length}, got {v.shape}")
+    if not np.all(np.isfinite(v)):
+        raise ValidationError(f"{name} contains non-finite entries")
+    return v
+
+
+class Solution:
+    """A primal-dual solution ``(x, y, s)``."""
+
+    __slots__ = ("x", "y", "s")
+
+    def __init__(self, x, y, s):
+        self.x = _vector("x", x)
+        self.y = _vector("y", y)
+        self.s = _vector("s", s, len(self.y))
+
+    n = property(lambda self: len(self.x))
+    m = property(lambda self: len(self.y))
+
+    def __repr__(self):
+        return f"Solution(n={self.n}, m={self.m})"
+
+
+class SolutionDelta:
+    """A direction ``(dx, dy, ds)`` in solution space."""
+
+    __slots__ = ("dx", "dy", "ds")
+
+    def __init__(self, dx, dy, ds):
+        self.dx = _vector("dx", dx)
+        self.dy = _vector("dy", dy)
+        self.ds = _vector("ds", ds, len(self.dy))
+
+    def dot(self, other):
+        return float(self.dx @ other.dx + self.dy @ other.dy + self.ds @ other.ds)
+
+    def norm(self):
+        return float(np.sqrt(self.dot(self)))
+
+    def __repr__(self):
+        return f"SolutionDelta(n={len(self.dx)}, m={len(self.dy)}, norm={self.norm():.3e})"
+
+
+@dataclass
+class KktReport:
+    """Optimality residuals of a candidate solution (solution_map.py:99-136)."""
+
+    primal: float
+    stationarity: float
+    gap: float
+    primal_cone_distance: float
+    dual_cone_distance: float
+    tol: float
+    ok: bool
+
+    def max_violation(self):
+        return max(self.primal, self.stationarity, self.gap, self.primal_cone_distance,
+                   self.dual_cone_distance)
+
+    def as_dict(self):
+        return {"primal": self.primal, "stationarity": self.stationarity, "gap": self.gap,
+                "primal_cone_distance": self.primal_cone_distance,
+                "dual_cone_distance": self.dual_cone_distance, "tol": self.tol, "ok": self.ok}
+
+
+@dataclass
+class Diagnostics:
+    """What happened inside a jvp / vjp (solution_map.py:139-167)."""
+
+    iterations: int
+    converged: bool
+    residual_norm: float
+    rhs_norm: float
+    derivative_unreliable: bool
+    kkt: Optional[KktReport]
+
+    def as_dict(self):
+        return {"iterations": self.iterations, "converged": self.converged,
+                "residual_norm": self.residual_norm, "rhs_norm": self.rhs_norm,
+                "derivative_unreliable": self.derivative_unreliable,
+                "kkt": None if self.kkt is None else self.kkt.as_dict()}
+
+
+def _diag(d, kkt=None):
+    return Diagnostics(int(d.iterations), bool(d.converged), float(d.residual_norm), float(d.rhs_norm),
+                       bool(d.derivative_unreliable), kkt)
+
+
+def _opts(atol, btol, max_iter):
+    o = N.LsmrOpts()
+    o.atol, o.btol = float(atol), float(btol)
+    # C ABI: 0 -> default cap 10*(in+out); < 0 -> an explicit cap of zero
+    o.max_iter = 0 if max_iter is None else (int(max_iter) if int(max_iter) > 0 else -1)
+    return o
+
+
+# ---------------------------------------------------------------------------
+# prepared handles
+# ---------------------------------------------------------------------------
+
+class QCPBatch:
+    """A batch of independent QCPs prepared on the GPU.
+
+    ``thetas``/``sols`` are sequences of ``ProblemData``/``Solution``.  All
+    kernels run once per LSMR iteration for the whole batch; converged
+    problems drop out via per-problem flags.
+    """
+
+    def __init__(self, thetas, sols):
+        import torch
+
+        thetas, sols = list(thetas), list(sols)
+        if len(thetas) != len(sols) or not thetas:
+            raise ValidationError("need equally many problems and solutions (at least one)")
+        for th, so in zip(thetas, sols):
+            if not isinstance(th, ProblemData):
+                raise ValidationError(f"theta must be a ProblemData, got {type(th).__name__}")
+            if not isinstance(so, Solution):
+                raise ValidationError(f"sol must be a Solution, got {type(so).__name__}")
+            if (so.n, so.m) != (th.n, th.m):
+                raise ValidationError(f"solution dimensions ({so.n}, {so.m}) do not match "
+                                      f"problem dimensions ({th.n}, {th.m})")
+        self.thetas, self.sols = thetas, sols
+        cat = lambda xs, dt=np.float64: np.concatenate([np.asarray(v, dtype=dt) for v in xs]) if xs else np.zeros(0, dt)
+        f64, i64 = torch.float64, torch.int64
+        dev = dict(
+            P_colptr=N.to_dev(cat([t.P.col_ptr for t in thetas], np.int64), i64),
+            P_rowidx=N.to_dev(cat([t.P.row_idx for t in thetas], np.int64), i64),
+            P_vals=N.to_dev(cat([t.P.values for t in thetas]), f64),
+            A_colptr=N.to_dev(cat([t.A.col_ptr for t in thetas], np.int64), i64),
+            A_rowidx=N.to_dev(cat([t.A.row_idx for t in thetas], np.int64), i64),
+            A_vals=N.to_dev(cat([t.A.values for t in thetas]), f64),
+            q=N.to_dev(cat([t.q for t in thetas]), f64), b=N.to_dev(cat([t.b for t in thetas]), f64),
+            x=N.to_dev(cat([s.x for s in sols]), f64), y=N.to_dev(cat([s.y for s in sols]), f64),
+            s=N.to_dev(cat([s.s for s in sols]), f64))
+        self._create([t.n for t in thetas], [t.m for t in thetas], [t.P.nnz for t in thetas],
+                     [t.A.nnz for t in thetas], [list(t.cone.blocks) for t in thetas], dev)
+        self._sol_dev = (dev["x"], dev["y"], dev["s"])
+
+    @classmethod
+    def from_device(cls, n, m, P_nnz, A_nnz, blocks, tensors):
+        """Create from concatenated CUDA tensors (keys as in ``qg_batch_desc``)."""
+        self = cls.__new__(cls)
+        self.thetas = self.sols = None
+        self._create(n, m, P_nnz, A_nnz, blocks, tensors)
+        self._sol_dev = (tensors["x"], tensors["y"], tensors["s"])
+        return self
+
+    def _create(self, n, m, P_nnz, A_nnz, blocks, t):
+        lib = N.lib()
+        self.B = len(n)
+        self.n, self.m = [int(v) for v in n], [int(v) for v in m]
+        self.P_nnz, self.A_nnz = [int(v) for v in P_nnz], [int(v) for v in A_nnz]
+        self.blocks = blocks
+        self.NX, self.NY = sum(self.n), sum(self.m)
+        self.xoff = np.concatenate([[0], np.cumsum(self.n)]).astype(np.int64)
+        self.yoff = np.concatenate([[0], np.cumsum(self.m)]).astype(np.int64)
+        self.poff = np.concatenate([[0], np.cumsum(self.P_nnz)]).astype(np.int64)
+        self.aoff = np.concatenate([[0], np.cumsum(self.A_nnz)]).astype(np.int64)
+        flat = [b for bl in blocks for b in bl]
+        keep = dict(n=N.i64_array(self.n), m=N.i64_array(self.m), pn=N.i64_array(self.P_nnz),
+                    an=N.i64_array(self.A_nnz), nb=N.i64_array([len(b) for b in blocks]),
+                    blk=N.cone_array(flat))
+        d = N.BatchDesc()
+        d.nprob = self.B
+        d.n, d.m, d.P_nnz, d.A_nnz, d.nblocks = keep["n"], keep["m"], keep["pn"], keep["an"], keep["nb"]
+        d.blocks = keep["blk"]
+        for k in ("P_colptr", "P_rowidx", "P_vals", "A_colptr", "A_rowidx", "A_vals", "q", "b", "x", "y", "s"):
+            setattr(d, k, t[k].data_ptr())
+        h = N.c_vp()
+        N.check(lib.qg_create_batch(N.ctypes.byref(h), N.ctypes.byref(d), N.stream_ptr()))
+        self._h, self._lib = h, lib
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.qg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device-level entry points ------------------------------------------
+    def jvp_device(self, dP_vals, dA_vals, dq, db, *, atol=1e-10, btol=1e-10, max_iter=None,
+                   dP_struct=None, dA_struct=None):
+        """jvp with CUDA inputs.  ``d*_vals`` on the patterns of P / A unless
+        ``dP_struct``/``dA_struct`` = (colptr, rowidx, nnz list) give others."""
+        lib = N.lib()
+        pc = N.PerturbationC()
+        keep = []
+        if dP_struct is None and dA_struct is None:
+            pc.same_pattern = 1
+            pc.dP_nnz, pc.dA_nnz = N.i64_array(self.P_nnz), N.i64_array(self.A_nnz)
+            keep += [pc.dP_nnz, pc.dA_nnz]
+        else:
+            pc.same_pattern = 0
+            (pcp, pri, pnz), (acp, ari, anz) = dP_struct, dA_struct
+            pc.dP_nnz, pc.dA_nnz = N.i64_array(pnz), N.i64_array(anz)
+            pc.dP_colptr, pc.dP_rowidx = pcp.data_ptr(), pri.data_ptr()
+            pc.dA_colptr, pc.dA_rowidx = acp.data_ptr(), ari.data_ptr()
+            keep += [pc.dP_nnz, pc.dA_nnz]
+        pc.dP_vals, pc.dA_vals = dP_vals.data_ptr(), dA_vals.data_ptr()
+        pc.dq, pc.db = dq.data_ptr(), db.data_ptr()
+        dx, dy, ds = N.empty(self.NX), N.empty(self.NY), N.empty(self.NY)
+        diags = (N.DiagC * self.B)()
+        o = _opts(atol, btol, max_iter)
+        N.check(lib.qg_jvp(self._h, N.ctypes.byref(pc), N.ctypes.byref(o), N.ptr(dx), N.ptr(dy), N.ptr(ds),
+                           diags, N.stream_ptr()))
+        return dx[:self.NX], dy[:self.NY], ds[:self.NY], list(diags)
+
+    def vjp_device(self, dx, dy, ds, *, atol=1e-10, btol=1e-10, max_iter=None):
+        lib = N.lib()
+        dP, dA = N.empty(self.poff[-1]), N.empty(self.aoff[-1])
+        dq, db = N.empty(self.NX), N.empty(self.NY)
+        diags = (N.DiagC * self.B)()
+        o = _opts(atol, btol, max_iter)
+        N.check(lib.qg_vjp(self._h, N.ptr(dx), N.ptr(dy), N.ptr(ds), N.ctypes.byref(o), N.ptr(dP), N.ptr(dA),
+                           N.ptr(dq), N.ptr(db), diags, N.stream_ptr()))
+        return dP[:self.poff[-1]], dA[:self.aoff[-1]], dq[:self.NX], db[:self.NY], list(diags)
+
+    def apply_F_device(self, w, transpose=False):
+        out = N.empty(self.NX + self.NY + self.B)
+        N.check(N.lib().qg_apply_F(self._h, 1 if transpose else 0, N.ptr(w), N.ptr(out), N.stream_ptr()))
+        return out
+
+    def embedding_point_device(self):
+        out = N.empty(self.NX + self.NY + self.B)
+        N.check(N.lib().qg_embedding_point(self._h, N.ptr(out), N.stream_ptr()))
+        return out
+
+    def kkt_device(self, x=None, y=None, s=None):
+        x0, y0, s0 = self._sol_dev
+        rep = (N.c_dbl * (5 * self.B))()
+        N.check(N.lib().qg_check(self._h, N.ptr(x if x is not None else x0), N.ptr(y if y is not None else y0),
+                                 N.ptr(s if s is not None else s0), rep, N.stream_ptr()))
+        return np.array(rep[:]).reshape(self.B, 5)
+
+    # -- host-level batch helpers --------------------------------------------
+    def _split(self, arr, off):
+        return [arr[off[i]:off[i + 1]] for i in range(self.B)]
+
+    def jvp_all(self, dthetas, **kw):
+        import torch
+
+        same = all(same_pattern(d.dP, t.P) and same_pattern(d.dA, t.A) for d, t in zip(dthetas, self.thetas))
+        cat = lambda xs: N.to_dev(np.concatenate(xs) if xs else np.zeros(0), torch.float64)
+        args = dict(dP_vals=cat([d.dP.values for d in dthetas]), dA_vals=cat([d.dA.values for d in dthetas]),
+                    dq=cat([d.dq for d in dthetas]), db=cat([d.db for d in dthetas]))
+        if not same:
+            i64 = lambda xs: N.to_dev(np.concatenate(xs), torch.int64)
+            args["dP_struct"] = (i64([d.dP.col_ptr for d in dthetas]), i64([d.dP.row_idx for d in dthetas]),
+                                 [d.dP.nnz for d in dthetas])
+            args["dA_struct"] = (i64([d.dA.col_ptr for d in dthetas]), i64([d.dA.row_idx for d in dthetas]),
+                                 [d.dA.nnz for d in dthetas])
+        dx, dy, ds, diags = self.jvp_device(**args, **kw)
+        dx, dy, ds = dx.cpu().numpy(), dy.cpu().numpy(), ds.cpu().numpy()
+        out = []
+        for i in range(self.B):
+            xs, ys = slice(self.xoff[i], self.xoff[i + 1]), slice(self.yoff[i], self.yoff[i + 1])
+            out.append((SolutionDelta(dx[xs], dy[ys], ds[ys]), _diag(diags[i])))
+        return out
+
+    def vjp_all(self, deltas, **kw):
+        import torch
+
+        cat = lambda xs: N.to_dev(np.concatenate(xs) if xs else np.zeros(0), torch.float64)
+        dP, dA, dq, db, diags = self.vjp_device(cat([d.dx for d in deltas]), cat([d.dy for d in deltas]),
+                                                cat([d.ds for d in deltas]), **kw)
+        dP, dA, dq, db = (t.cpu().numpy() for t in (dP, dA, dq, db))
+        out = []
+        for i, th in enumerate(self.thetas):
+            g = DataPerturbation(th.P.with_values(dP[self.poff[i]:self.poff[i + 1]]),
+                                 th.A.with_values(dA[self.aoff[i]:self.aoff[i + 1]]),
+                                 dq[self.xoff[i]:self.xoff[i + 1]], db[self.yoff[i]:self.yoff[i + 1]],
+                                 _trusted=True)
+            out.append((g, _diag(diags[i])))
+        return out
+
+
+class QCP(QCPBatch):
+    """Prepared derivative of one QCP's solution map at ``sol``."""
+
+    def __init__(self, theta, sol):
+        super().__init__([theta], [sol])
+        self.theta, self.sol = theta, sol
+
+    def jvp(self, dtheta, *, atol=1e-10, btol=1e-10, max_iter=None):
+        _check_dtheta(self.theta, dtheta)
+        (delta, diag), = self.jvp_all([dtheta], atol=atol, btol=btol, max_iter=max_iter)
+        return delta, diag
+
+    def vjp(self, delta, *, atol=1e-10, btol=1e-10, max_iter=None):
+        _check_delta(self.theta, delta)
+        (grad, diag), = self.vjp_all([delta], atol=atol, btol=btol, max_iter=max_iter)
+        return grad, diag
+
+    def apply_F(self, w, transpose=False):
+        """``F w`` / ``F' w`` (embedding.py:420-425), host vectors."""
+        import torch
+
+        w = _vector("w", w, self.theta.embedding_dim)
+        return self.apply_F_device(N.to_dev(w, torch.float64), transpose)[:w.size].cpu().numpy()
+
+    def embedding_point(self):
+        return self.embedding_point_device()[:self.theta.embedding_dim].cpu().numpy()
+
+    def kkt(self, tol=None):
+        r = self.kkt_device()[0]
+        tol = float(1e-6 * (1.0 + self.theta.norm()) if tol is None else tol)
+        return KktReport(*(float(v) for v in r), tol, bool(max(r) <= tol))
+
+
+# ---------------------------------------------------------------------------
+# reference-compatible functions
+# ---------------------------------------------------------------------------
+
+def _check_dtheta(theta, dtheta):
+    if not isinstance(dtheta, DataPerturbation):
+        raise ValidationError(f"dtheta must be a DataPerturbation, got {type(dtheta).__name__}")
+    if (dtheta.n, dtheta.m) != (theta.n, theta.m):
+        raise ValidationError(f"perturbation dimensions ({dtheta.n}, {dtheta.m}) do not match "
+                              f"problem dimensions ({theta.n}, {theta.m})")
+
+
+def _check_delta(theta, delta):
+    if not isinstance(delta, SolutionDelta):
+        raise ValidationError(f"delta must be a SolutionDelta, got {type(delta).__name__}")
+    if (len(delta.dx), len(delta.dy)) != (theta.n, theta.m):
+        raise ValidationError(f"delta dimensions ({len(delta.dx)}, {len(delta.dy)}) do not match "
+                              f"problem dimensions ({theta.n}, {theta.m})")
+
+
+def _check_sol(theta, sol):
+    if not isinstance(sol, Solution):
+        raise ValidationError(f"sol must be a Solution, got {type(sol).__name__}")
+    if (sol.n, sol.m) != (theta.n, theta.m):
+        raise ValidationError(f"solution dimensions ({sol.n}, {sol.m}) do not match "
+                              f"problem dimensions ({theta.n}, {theta.m})")
+
+
+def embed(sol):
+    """``z = (x, y - s, 1)`` (solution_map.py:170-179)."""
+    return np.concatenate([sol.x, sol.y - sol.s, [1.0]])
+
+
+def phi(theta, z):
+    """Decode an embedding point (solution_map.py:182-194); projection on GPU."""
+    z = _vector("z", z, theta.embedding_dim)
+    zN = z[-1]
+    if zN <= 0.0:
+        raise DomainError(f"decoding needs z_N > 0, got {zN}")
+    mid = z[theta.n:-1]
+    proj = cones.project_dual(theta.cone, mid)
+    return Solution(z[:theta.n] / zN, proj / zN, (proj - mid) / zN)
+
+
+def check_solution(theta, sol, tol=None):
+    """KKT residuals of ``sol`` (solution_map.py:263-288), on the GPU."""
+    _check_sol(theta, sol)
+    return QCP(theta, sol).kkt(tol)
+
+
+def _prepare(theta, sol, check, check_tol):
+    _check_sol(theta, sol)
+    q = QCP(theta, sol)
+    report = None
+    if check:
+        report = q.kkt(check_tol)
+        if not report.ok:
+            exc = ValidationError("solution fails the optimality pre-check: "
+                                  f"max violation {report.max_violation():.3e} > tolerance {report.tol:.3e} "
+                                  "(pass check=False to differentiate anyway)")
+            exc.kkt = report
+            raise exc
+    return q, report
+
+
+def jvp(theta, sol, dtheta, *, atol=1e-10, btol=1e-10, max_iter=None, check=True, check_tol=None):
+    """Directional derivative of the solution map (solution_map.py:325-355)."""
+    q, report = _prepare(theta, sol, check, check_tol)
+    try:
+        delta, diag = q.jvp(dtheta, atol=atol, btol=btol, max_iter=max_iter)
+    finally:
+        q.close()
+    diag.kkt = report
+    return delta, diag
+
+
+def vjp(theta, sol, delta, *, atol=1e-10, btol=1e-10, max_iter=None, check=True, check_tol=None):
+    """Adjoint of the solution-map derivative (solution_map.py:358-385)."""
+    q, report = _prepare(theta, sol, check, check_tol)
+    try:
+        grad, diag = q.vjp(delta, atol=atol, btol=btol, max_iter=max_iter)
+    finally:
+        q.close()
+    diag.kkt = report
+    return grad, diag

@@ -61,3 +61,37 @@ def kat_block(tag):
 def kat_tags():
     d = load("cones_kat.npz")
     return sorted({k.split("__")[0] for k in d})
+
+
+def product_instance(d):
+    """The same fixture as product objects (paper_2508_17522_b200)."""
+    import paper_2508_17522_b200 as qg
+
+    def m(prefix):
+        r, c = (int(v) for v in d[f"{prefix}_shape"])
+        return qg.CscMatrix(r, c, d[f"{prefix}_colptr"], d[f"{prefix}_rowidx"], d[f"{prefix}_vals"])
+
+    blks = []
+    for k, dim, order, alpha in zip(d["cone_kind"], d["cone_dim"], d["cone_order"], d["cone_alpha"]):
+        kind = KINDS[int(k)]
+        blks.append(qg.ConeBlock(kind, dim=int(dim)) if kind in ("zero", "nonneg", "soc") else
+                    qg.ConeBlock(kind, order=int(order)) if kind == "psd" else
+                    qg.ConeBlock(kind, alpha=float(alpha)) if kind in ("pow", "dpow") else qg.ConeBlock(kind))
+    theta = qg.ProblemData(m("P"), m("A"), d["q"], d["b"], qg.ConeSpec(blks))
+    sol = qg.Solution(d["x"], d["y"], d["s"])
+    pert = qg.DataPerturbation(m("dP"), m("dA"), d["dq"], d["db"])
+    delta = qg.SolutionDelta(d["dx"], d["dy"], d["ds"])
+    return theta, sol, pert, delta
+
+
+def product_block(tag):
+    import paper_2508_17522_b200 as qg
+
+    kind, _, alpha = tag.partition("_")
+    if kind == "psd":
+        return qg.ConeBlock.psd(3)
+    if kind in ("pow", "dpow"):
+        return qg.ConeBlock(kind, alpha=float(alpha))
+    if kind in ("exp", "dexp"):
+        return qg.ConeBlock(kind)
+    return qg.ConeBlock(kind, dim=5)

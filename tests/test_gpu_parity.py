@@ -1,0 +1,140 @@
+"""Parity of the CUDA path (through the C ABI) with the reference.
+
+Fixtures come from the real reference (tests/golden/make_fixtures.py); the
+oracle (oracle/) supplies the same quantities for instances built here.
+Tolerances are the north star's: cone projections and D Pi <= 1e-12
+relative, jvp/vjp <= 1e-6 relative at matched LSMR tolerance / cap.
+"""
+
+import numpy as np
+import pytest
+
+from fixtures import KINDS, gap, instance, kat_tags, load, product_block, product_instance
+
+pytestmark = pytest.mark.gpu
+
+qg = pytest.importorskip("paper_2508_17522_b200")
+
+
+@pytest.mark.parametrize("tag", kat_tags())
+def test_cone_calculus_matches_reference(tag):
+    d = load("cones_kat.npz")
+    b = product_block(tag)
+    spec = qg.ConeSpec([b])
+    for row, pp, pd, dd, dp, ok in zip(d[f"{tag}__pts"], d[f"{tag}__proj"], d[f"{tag}__projdual"],
+                                       d[f"{tag}__dprojdual"], d[f"{tag}__dproj"], d[f"{tag}__ok"]):
+        p, dirs = row[:b.dim], row[b.dim:].reshape(2, b.dim)
+        if not ok:
+            with pytest.raises(qg.ConegradError):
+                qg.project(spec, p)
+                qg.project_dual(spec, p)
+                qg.dprojection_dual(spec, p)
+                qg.dprojection(spec, p)
+            continue
+        assert gap(qg.project(spec, p), pp) <= 1e-12, (tag, p)
+        assert gap(qg.project_dual(spec, p), pd) <= 1e-12, (tag, p)
+        Dd, Dp = qg.dprojection_dual(spec, p), qg.dprojection(spec, p)
+        for e, want_d, want_p in zip(dirs, dd, dp):
+            assert gap(Dd.matvec(e), want_d) <= 1e-12, (tag, p)
+            assert gap(Dp.matvec(e), want_p) <= 1e-12, (tag, p)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_operator_matches_reference(kind):
+    d = load(f"golden_{kind}.npz")
+    theta, sol, _, _ = product_instance(d)
+    q = qg.QCP(theta, sol)
+    assert gap(q.embedding_point(), d["op_pz"]) <= 1e-12
+    for w, fw, ftw in zip(d["op_w"], d["op_Fw"], d["op_FTw"]):
+        assert gap(q.apply_F(w), fw) <= 1e-12
+        assert gap(q.apply_F(w, transpose=True), ftw) <= 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_fixed_cap_jvp_vjp_match_reference(kind):
+    d = load(f"golden_{kind}.npz")
+    theta, sol, pert, delta = product_instance(d)
+    q = qg.QCP(theta, sol)
+    dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=20)
+    assert dg.iterations == d["k20_jvp_its"]
+    assert max(gap(dl.dx, d["k20_jvp_dx"]), gap(dl.dy, d["k20_jvp_dy"]), gap(dl.ds, d["k20_jvp_ds"])) <= 1e-6
+    g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=20)
+    assert vg.iterations == d["k20_vjp_its"]
+    assert max(gap(g.dP.values, d["k20_vjp_dP"]), gap(g.dA.values, d["k20_vjp_dA"]),
+               gap(g.dq, d["k20_vjp_dq"]), gap(g.db, d["k20_vjp_db"])) <= 1e-6
+
+
+@pytest.mark.parametrize("kind", ["soc", "psd", "exp", "dexp", "pow", "dpow"])
+def test_golden_converged_outputs(kind):
+    # goldens are reachable to ~1e-10..7e-9 by any implementation
+    # with a different summation order; zero / nonneg are ill-conditioned.
+    d = load(f"golden_{kind}.npz")
+    theta, sol, pert, delta = product_instance(d)
+    dl, dg = qg.jvp(theta, sol, pert)
+    assert abs(dg.iterations - int(d["jvp_its"])) <= 3
+    assert dg.converged and not dg.derivative_unreliable
+    assert max(gap(dl.dx, d["jvp_dx"]), gap(dl.dy, d["jvp_dy"]), gap(dl.ds, d["jvp_ds"])) <= 1e-6
+    g, vg = qg.vjp(theta, sol, delta)
+    assert abs(vg.iterations - int(d["vjp_its"])) <= 3
+    assert max(gap(g.dP.values, d["vjp_dP"]), gap(g.dA.values, d["vjp_dA"]),
+               gap(g.dq, d["vjp_dq"]), gap(g.db, d["vjp_db"])) <= 1e-6
+    assert np.array_equal(g.dP.col_ptr, theta.P.col_ptr) and np.array_equal(g.dA.row_idx, theta.A.row_idx)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_vjp_dP_exactly_symmetric(kind):
+    # reference tests/test_solution_map.py:396-410 (atol = 0)
+    d = load(f"golden_{kind}.npz")
+    theta, sol, _, delta = product_instance(d)
+    g, _ = qg.vjp(theta, sol, delta, check=False)
+    D = g.dP.to_dense()
+    assert np.array_equal(D, D.T)
+
+
+def test_c1ref_fixed_cap():
+    d = load("c1ref.npz")
+    theta, sol, pert, delta = product_instance(d)
+    q = qg.QCP(theta, sol)
+    for K in (20, 200):
+        dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=K)
+        assert dg.iterations == d[f"k{K}_jvp_its"]
+        assert max(gap(dl.dx, d[f"k{K}_jvp_dx"]), gap(dl.dy, d[f"k{K}_jvp_dy"])) <= 1e-6
+        g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=K)
+        assert vg.iterations == d[f"k{K}_vjp_its"]
+        assert max(gap(g.dP.values, d[f"k{K}_vjp_dP"]), gap(g.dA.values, d[f"k{K}_vjp_dA"])) <= 1e-6
+    for w, fw, ftw in zip(d["op_w"], d["op_Fw"], d["op_FTw"]):
+        assert gap(q.apply_F(w), fw) <= 1e-12
+        assert gap(q.apply_F(w, transpose=True), ftw) <= 1e-12
+
+
+def test_kkt_precheck_matches_reference():
+    for kind in KINDS:
+        d = load(f"golden_{kind}.npz")
+        theta, sol, _, _ = product_instance(d)
+        rep = qg.check_solution(theta, sol)
+        assert rep.ok
+        got = np.array([rep.primal, rep.stationarity, rep.gap, rep.primal_cone_distance, rep.dual_cone_distance])
+        assert np.all(np.abs(got - d["kkt"]) <= 1e-12 * (1 + np.abs(d["kkt"]).max()))
+
+
+def test_batch_equals_singles():
+    items = [product_instance(load(f"golden_{k}.npz")) for k in KINDS]
+    batch = qg.QCPBatch([t for t, _, _, _ in items], [s for _, s, _, _ in items])
+    outs = batch.jvp_all([p for _, _, p, _ in items], atol=0.0, btol=0.0, max_iter=20)
+    for (theta, sol, pert, _), (dl, dg) in zip(items, outs):
+        one, og = qg.QCP(theta, sol).jvp(pert, atol=0.0, btol=0.0, max_iter=20)
+        assert dg.iterations == og.iterations
+        assert gap(dl.dx, one.dx) <= 1e-12 and gap(dl.dy, one.dy) <= 1e-12
+    vouts = batch.vjp_all([de for _, _, _, de in items], atol=0.0, btol=0.0, max_iter=20)
+    for (theta, sol, _, de), (g, vg) in zip(items, vouts):
+        one, og = qg.QCP(theta, sol).vjp(de, atol=0.0, btol=0.0, max_iter=20)
+        assert gap(g.dA.values, one.dA.values) <= 1e-12 and gap(g.dq, one.dq) <= 1e-12
+
+
+def test_deterministic_repeat():
+    d = load("golden_psd.npz")
+    theta, sol, pert, _ = product_instance(d)
+    q = qg.QCP(theta, sol)
+    a, _ = q.jvp(pert)
+    b, _ = q.jvp(pert)
+    assert np.array_equal(a.dx, b.dx) and np.array_equal(a.ds, b.ds)
