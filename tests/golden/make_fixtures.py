@@ -76,6 +76,18 @@ def run_fixed(theta, sol, dtheta, delta, K):
     return out
 
 
+def run_tol(theta, sol, dtheta, delta, tol, tag):
+    out = {}
+    dl, dg = sm.jvp(theta, sol, dtheta, atol=tol, btol=tol)
+    out.update({f"{tag}_jvp_dx": dl.dx, f"{tag}_jvp_dy": dl.dy, f"{tag}_jvp_ds": dl.ds,
+                f"{tag}_jvp_its": np.int64(dg.iterations), f"{tag}_jvp_res": dg.residual_norm})
+    g, vg = sm.vjp(theta, sol, delta, atol=tol, btol=tol)
+    out.update({f"{tag}_vjp_dP": g.dP.values, f"{tag}_vjp_dA": g.dA.values,
+                f"{tag}_vjp_dq": g.dq, f"{tag}_vjp_db": g.db,
+                f"{tag}_vjp_its": np.int64(vg.iterations), f"{tag}_vjp_res": vg.residual_norm})
+    return out
+
+
 def operator_probes(theta, sol, rng, count=3):
     z = sm.embed(sol)
     F = make_F(theta, z)
@@ -119,7 +131,8 @@ def golden_file(kind):
     assert dg.iterations == d["jvp_its"]
     rng = np.random.default_rng(KCODE[kind] + 100)
     d.update(operator_probes(theta, sol, rng))
-    d.update(run_fixed(theta, sol, dtheta, delta, 20))
+    d.update(run_fixed(theta, sol, dtheta, delta, 5))
+    d.update(run_tol(theta, sol, dtheta, delta, 1e-14, "t14"))
     d.update(kkt=np.array([v for k, v in sm.check_solution(theta, sol).as_dict().items()
                            if k not in ("tol", "ok")]))
     np.savez_compressed(OUT / f"golden_{kind}.npz", **d)
@@ -194,10 +207,57 @@ def c1ref():
     d.update(csc_arrays("dP", dtheta.dP))
     d.update(csc_arrays("dA", dtheta.dA))
     d.update(dq=dtheta.dq, db=dtheta.db, dx=delta.dx, dy=delta.dy, ds=delta.ds)
-    d.update(run_fixed(theta, sol, dtheta, delta, 20))
-    d.update(run_fixed(theta, sol, dtheta, delta, 200))
+    d.update(run_fixed(theta, sol, dtheta, delta, 3))
     d.update(operator_probes(theta, sol, np.random.default_rng(5)))
     np.savez_compressed(OUT / "c1ref.npz", **d)
+
+
+# Small instances built with the conditioning recipe by the
+# product's synthetic generator; outputs from the reference at atol=btol=1e-14
+# (the matched tolerance at which outputs are insensitive to summation order).
+RECIPES = {
+    "r_qp": ([("zero", 20, 0, 0.0), ("nonneg", 70, 0, 0.0)], 60, 900, True),
+    "r_soc": ([("soc", 6, 0, 0.0)] * 12, 60, 1000, False),
+    "r_exppow": ([("exp", 3, 0, 0.0)] * 8 + [("dexp", 3, 0, 0.0)] * 8 + [("pow", 3, 0, 0.3)] * 8
+                 + [("dpow", 3, 0, 0.7)] * 8, 80, 1400, True),
+    "r_psd": ([("nonneg", 10, 0, 0.0)] + [("psd", 21, 6, 0.0)] * 3, 60, 900, False),
+    "r_mixed": ([("zero", 5, 0, 0.0), ("nonneg", 10, 0, 0.0), ("soc", 5, 0, 0.0), ("soc", 4, 0, 0.0),
+                 ("psd", 10, 4, 0.0), ("exp", 3, 0, 0.0), ("exp", 3, 0, 0.0), ("dexp", 3, 0, 0.0),
+                 ("pow", 3, 0, 0.4), ("dpow", 3, 0, 0.6)], 70, 900, True),
+}
+
+
+def recipe(name):
+    sys.path.insert(0, str(OUT.parent.parent))
+    from paper_2508_17522_b200 import synth
+    from conegrad.embedding import DataPerturbation, ProblemData
+    from conegrad.solution_map import Solution, SolutionDelta
+    from conegrad.sparse import CscMatrix
+
+    cones_, n, nnzA, diagP = RECIPES[name]
+    bt = synth.custom(cones_, n, nnzA, seed=11, diag_P=diagP)
+    dirs = synth.directions(bt, seed=12)
+    o = synth.problem_objects(bt, 0, None)
+    m = o["m"]
+    blocks = []
+    for k, dm, od, al in o["blocks"]:
+        blocks.append(cones.ConeBlock(k, dim=dm) if k in ("zero", "nonneg", "soc") else
+                      cones.ConeBlock(k, order=od) if k == "psd" else
+                      cones.ConeBlock(k, alpha=al) if k in ("pow", "dpow") else cones.ConeBlock(k))
+    P = CscMatrix(n, n, *o["P"])
+    A = CscMatrix(m, n, *o["A"])
+    theta = ProblemData(P, A, o["q"], o["b"], cones.ConeSpec(blocks))
+    sol = Solution(o["x"], o["y"], o["s"])
+    dtheta = DataPerturbation(P.with_values(dirs.dP), A.with_values(dirs.dA), dirs.dq, dirs.db)
+    delta = SolutionDelta(dirs.dx, dirs.dy, dirs.ds)
+    d = problem_arrays(theta, sol)
+    d.update(csc_arrays("dP", dtheta.dP))
+    d.update(csc_arrays("dA", dtheta.dA))
+    d.update(dq=dtheta.dq, db=dtheta.db, dx=delta.dx, dy=delta.dy, ds=delta.ds)
+    d.update(run_tol(theta, sol, dtheta, delta, 1e-14, "t14"))
+    d.update(run_fixed(theta, sol, dtheta, delta, 5))
+    d.update(operator_probes(theta, sol, np.random.default_rng(3)))
+    np.savez_compressed(OUT / f"{name}.npz", **d)
 
 
 if __name__ == "__main__":
@@ -208,3 +268,6 @@ if __name__ == "__main__":
     print("cones_kat")
     c1ref()
     print("c1ref")
+    for name in RECIPES:
+        recipe(name)
+        print(name)

@@ -1,19 +1,36 @@
 """Parity of the CUDA path (through the C ABI) with the reference.
 
-Fixtures come from the real reference (tests/golden/make_fixtures.py); the
-oracle (oracle/) supplies the same quantities for instances built here.
+Fixtures come from the real reference (tests/golden/make_fixtures.py).
 Tolerances are the north star's: cone projections and D Pi <= 1e-12
-relative, jvp/vjp <= 1e-6 relative at matched LSMR tolerance / cap.
+relative; jvp/vjp <= 1e-6 relative at a matched LSMR tolerance and cap.
+
+Which caps are comparable at all (measured with the oracle, see DESIGN.md
+"Parity protocol"): these small instances make F rank-deficient (F z = 0)
+and ill-conditioned, so LSMR iterates at intermediate caps amplify 1-ulp
+input noise to 1e-4..1e-1 *inside the reference itself*.  Outputs are
+insensitive (<= 1e-11) at K <= 5 and at convergence with atol=btol=1e-14
+(<= 2e-7 for every golden, <= 1e-9 on recipe-conditioned instances); those
+are the matched settings used here.
 """
 
 import numpy as np
 import pytest
 
-from fixtures import KINDS, gap, instance, kat_tags, load, product_block, product_instance
+from fixtures import KINDS, gap, kat_tags, load, product_block, product_instance
 
 pytestmark = pytest.mark.gpu
 
 qg = pytest.importorskip("paper_2508_17522_b200")
+RECIPES = ["r_qp", "r_soc", "r_exppow", "r_psd", "r_mixed"]
+
+
+def _jvp_gap(dl, d, tag):
+    return max(gap(dl.dx, d[f"{tag}_jvp_dx"]), gap(dl.dy, d[f"{tag}_jvp_dy"]), gap(dl.ds, d[f"{tag}_jvp_ds"]))
+
+
+def _vjp_gap(g, d, tag):
+    return max(gap(g.dP.values, d[f"{tag}_vjp_dP"]), gap(g.dA.values, d[f"{tag}_vjp_dA"]),
+               gap(g.dq, d[f"{tag}_vjp_dq"]), gap(g.db, d[f"{tag}_vjp_db"]))
 
 
 @pytest.mark.parametrize("tag", kat_tags())
@@ -39,9 +56,9 @@ def test_cone_calculus_matches_reference(tag):
             assert gap(Dp.matvec(e), want_p) <= 1e-12, (tag, p)
 
 
-@pytest.mark.parametrize("kind", KINDS)
-def test_operator_matches_reference(kind):
-    d = load(f"golden_{kind}.npz")
+@pytest.mark.parametrize("name", [f"golden_{k}" for k in KINDS] + RECIPES + ["c1ref"])
+def test_operator_matches_reference(name):
+    d = load(f"{name}.npz")
     theta, sol, _, _ = product_instance(d)
     q = qg.QCP(theta, sol)
     assert gap(q.embedding_point(), d["op_pz"]) <= 1e-12
@@ -50,29 +67,40 @@ def test_operator_matches_reference(kind):
         assert gap(q.apply_F(w, transpose=True), ftw) <= 1e-12
 
 
-@pytest.mark.parametrize("kind", KINDS)
-def test_fixed_cap_jvp_vjp_match_reference(kind):
-    d = load(f"golden_{kind}.npz")
+@pytest.mark.parametrize("name", [f"golden_{k}" for k in KINDS] + RECIPES)
+def test_fixed_cap_matches_reference(name):
+    d = load(f"{name}.npz")
     theta, sol, pert, delta = product_instance(d)
     q = qg.QCP(theta, sol)
-    dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=20)
-    assert dg.iterations == d["k20_jvp_its"]
-    assert max(gap(dl.dx, d["k20_jvp_dx"]), gap(dl.dy, d["k20_jvp_dy"]), gap(dl.ds, d["k20_jvp_ds"])) <= 1e-6
-    g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=20)
-    assert vg.iterations == d["k20_vjp_its"]
-    assert max(gap(g.dP.values, d["k20_vjp_dP"]), gap(g.dA.values, d["k20_vjp_dA"]),
-               gap(g.dq, d["k20_vjp_dq"]), gap(g.db, d["k20_vjp_db"])) <= 1e-6
+    dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=5)
+    assert dg.iterations == d["k5_jvp_its"]
+    assert _jvp_gap(dl, d, "k5") <= 1e-6
+    g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=5)
+    assert vg.iterations == d["k5_vjp_its"]
+    assert _vjp_gap(g, d, "k5") <= 1e-6
+
+
+@pytest.mark.parametrize("name", [f"golden_{k}" for k in KINDS] + RECIPES)
+def test_matched_tolerance_matches_reference(name):
+    d = load(f"{name}.npz")
+    theta, sol, pert, delta = product_instance(d)
+    dl, dg = qg.jvp(theta, sol, pert, atol=1e-14, btol=1e-14)
+    assert abs(dg.iterations - int(d["t14_jvp_its"])) <= max(3, int(0.05 * d["t14_jvp_its"]))
+    assert _jvp_gap(dl, d, "t14") <= 1e-6
+    g, vg = qg.vjp(theta, sol, delta, atol=1e-14, btol=1e-14)
+    assert abs(vg.iterations - int(d["t14_vjp_its"])) <= max(3, int(0.05 * d["t14_vjp_its"]))
+    assert _vjp_gap(g, d, "t14") <= 1e-6
 
 
 @pytest.mark.parametrize("kind", ["soc", "psd", "exp", "dexp", "pow", "dpow"])
-def test_golden_converged_outputs(kind):
-    # goldens are reachable to ~1e-10..7e-9 by any implementation
-    # with a different summation order; zero / nonneg are ill-conditioned.
+def test_golden_default_tolerance(kind):
+    # the reference's own frozen outputs at its default tolerance 1e-10
+    # (reachable to <= 7e-9 by any summation order)
     d = load(f"golden_{kind}.npz")
     theta, sol, pert, delta = product_instance(d)
     dl, dg = qg.jvp(theta, sol, pert)
     assert abs(dg.iterations - int(d["jvp_its"])) <= 3
-    assert dg.converged and not dg.derivative_unreliable
+    assert dg.converged == bool(d["jvp_conv"]) and dg.derivative_unreliable == bool(d["jvp_unrel"])
     assert max(gap(dl.dx, d["jvp_dx"]), gap(dl.dy, d["jvp_dy"]), gap(dl.ds, d["jvp_ds"])) <= 1e-6
     g, vg = qg.vjp(theta, sol, delta)
     assert abs(vg.iterations - int(d["vjp_its"])) <= 3
@@ -91,20 +119,14 @@ def test_vjp_dP_exactly_symmetric(kind):
     assert np.array_equal(D, D.T)
 
 
-def test_c1ref_fixed_cap():
+def test_c1ref_small_cap():
     d = load("c1ref.npz")
     theta, sol, pert, delta = product_instance(d)
     q = qg.QCP(theta, sol)
-    for K in (20, 200):
-        dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=K)
-        assert dg.iterations == d[f"k{K}_jvp_its"]
-        assert max(gap(dl.dx, d[f"k{K}_jvp_dx"]), gap(dl.dy, d[f"k{K}_jvp_dy"])) <= 1e-6
-        g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=K)
-        assert vg.iterations == d[f"k{K}_vjp_its"]
-        assert max(gap(g.dP.values, d[f"k{K}_vjp_dP"]), gap(g.dA.values, d[f"k{K}_vjp_dA"])) <= 1e-6
-    for w, fw, ftw in zip(d["op_w"], d["op_Fw"], d["op_FTw"]):
-        assert gap(q.apply_F(w), fw) <= 1e-12
-        assert gap(q.apply_F(w, transpose=True), ftw) <= 1e-12
+    dl, dg = q.jvp(pert, atol=0.0, btol=0.0, max_iter=3)
+    assert dg.iterations == 3 and _jvp_gap(dl, d, "k3") <= 1e-6
+    g, vg = q.vjp(delta, atol=0.0, btol=0.0, max_iter=3)
+    assert vg.iterations == 3 and _vjp_gap(g, d, "k3") <= 1e-6
 
 
 def test_kkt_precheck_matches_reference():
@@ -117,17 +139,26 @@ def test_kkt_precheck_matches_reference():
         assert np.all(np.abs(got - d["kkt"]) <= 1e-12 * (1 + np.abs(d["kkt"]).max()))
 
 
+def test_precheck_rejects_bad_solution():
+    d = load("golden_soc.npz")
+    theta, sol, pert, _ = product_instance(d)
+    bad = qg.Solution(sol.x + 1.0, sol.y, sol.s)
+    with pytest.raises(qg.ValidationError) as exc:
+        qg.jvp(theta, bad, pert)
+    assert not exc.value.kkt.ok
+
+
 def test_batch_equals_singles():
     items = [product_instance(load(f"golden_{k}.npz")) for k in KINDS]
     batch = qg.QCPBatch([t for t, _, _, _ in items], [s for _, s, _, _ in items])
-    outs = batch.jvp_all([p for _, _, p, _ in items], atol=0.0, btol=0.0, max_iter=20)
+    outs = batch.jvp_all([p for _, _, p, _ in items], atol=1e-14, btol=1e-14)
     for (theta, sol, pert, _), (dl, dg) in zip(items, outs):
-        one, og = qg.QCP(theta, sol).jvp(pert, atol=0.0, btol=0.0, max_iter=20)
+        one, og = qg.QCP(theta, sol).jvp(pert, atol=1e-14, btol=1e-14)
         assert dg.iterations == og.iterations
         assert gap(dl.dx, one.dx) <= 1e-12 and gap(dl.dy, one.dy) <= 1e-12
-    vouts = batch.vjp_all([de for _, _, _, de in items], atol=0.0, btol=0.0, max_iter=20)
+    vouts = batch.vjp_all([de for _, _, _, de in items], atol=1e-14, btol=1e-14)
     for (theta, sol, _, de), (g, vg) in zip(items, vouts):
-        one, og = qg.QCP(theta, sol).vjp(de, atol=0.0, btol=0.0, max_iter=20)
+        one, og = qg.QCP(theta, sol).vjp(de, atol=1e-14, btol=1e-14)
         assert gap(g.dA.values, one.dA.values) <= 1e-12 and gap(g.dq, one.dq) <= 1e-12
 
 
@@ -138,3 +169,14 @@ def test_deterministic_repeat():
     a, _ = q.jvp(pert)
     b, _ = q.jvp(pert)
     assert np.array_equal(a.dx, b.dx) and np.array_equal(a.ds, b.ds)
+
+
+def test_zero_rhs_and_zero_cap():
+    d = load("golden_soc.npz")
+    theta, sol, pert, _ = product_instance(d)
+    q = qg.QCP(theta, sol)
+    zero = qg.DataPerturbation.zeros_like(theta)
+    dl, dg = q.jvp(zero)
+    assert dg.iterations == 0 and dg.converged and np.all(dl.dx == 0)
+    dl, dg = q.jvp(pert, max_iter=0)
+    assert dg.iterations == 0 and not dg.converged
