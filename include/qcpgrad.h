@@ -142,6 +142,12 @@ int qg_spmv_csc(int64_t nrows, int64_t ncols, const int64_t *col_ptr, const int6
                 const double *values, int64_t nnz, int adjoint, const double *x, double *out,
                 void *stream);
 
+/* Benchmark hook: launch one hot-path kernel of the prepared batch -- which =
+ * 0: fused F step (SpMV + epilogue), 1: fused F' step (SpMV + D Pi epilogues),
+ * 2: LSMR vector update -- `reps` times on `stream` between CUDA events;
+ * *avg_ms receives the mean device time per launch. */
+int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stream);
+
 /* Number of kernels this library launched since load (telemetry). */
 int64_t qg_kernel_launches(void);
 

@@ -80,6 +80,7 @@ _SIGS = {
     "qg_cones_project": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "qg_cones_prepare": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_vp]),
     "qg_cones_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
+    "qg_time_kernel": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_dbl), c_vp]),
     "qg_spmv_csc": (ctypes.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp]),
 }
 

@@ -523,6 +523,58 @@ int qg_spmv_csc(int64_t nrows, int64_t ncols, const int64_t *col_ptr, const int6
   QG_API_END
 }
 
+int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  // deterministic finite inputs: v = 1/sqrt(NE), u = v (D Pi v from the prepared derivative)
+  std::vector<double> ones(H.NE, 1.0 / std::sqrt((double)std::max<int64_t>(H.NE, 1)));
+  QG_CUDA(cudaMemcpyAsync(W.v, ones.data(), sizeof(double) * H.NE, cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(W.u, ones.data(), sizeof(double) * H.NE, cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(W.h, ones.data(), sizeof(double) * H.NE, cudaMemcpyHostToDevice, st));
+  H.cones.apply(W.v + H.NX, W.dpv, st);
+  // a state in which every problem is active with unit coefficients
+  std::vector<Lsmr> L(H.B);
+  for (auto &l : L) {
+    l = Lsmr{};
+    l.active = 1;
+    l.s_in = 1.0; l.c_out = 0.5; l.s_v = 1.0;
+    l.c_hbar = 0.25; l.c_x = 0.5; l.c_h = 0.125;
+  }
+  QG_CUDA(cudaMemcpyAsync(W.st, L.data(), sizeof(Lsmr) * H.B, cudaMemcpyHostToDevice, st));
+  auto launch = [&]() {
+    if (which == 0) {
+      StepArgs a{W.v, W.dpv, W.u, W.u, nullptr, W.tY, W.tY2, W.st, 0, W.part};
+      launch_step(H, M, STEP_F, a, st);
+    } else if (which == 1) {
+      StepArgs a{W.u, W.dpu, W.v, W.v, W.dpv, W.tY, W.tY2, W.st, 0, W.part};
+      launch_step(H, M, STEP_FT, a, st);
+    } else {
+      UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
+      launch_update(H, M, ua, st);
+    }
+  };
+  QG_CUDA(cudaMemsetAsync(W.hb, 0, sizeof(double) * H.NE, st));
+  QG_CUDA(cudaMemsetAsync(W.x, 0, sizeof(double) * H.NE, st));
+  for (int i = 0; i < 3; ++i) launch();
+  cudaEvent_t e0, e1;
+  QG_CUDA(cudaEventCreate(&e0));
+  QG_CUDA(cudaEventCreate(&e1));
+  QG_CUDA(cudaEventRecord(e0, st));
+  for (int i = 0; i < reps; ++i) launch();
+  QG_CUDA(cudaEventRecord(e1, st));
+  QG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  QG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *avg_ms = (double)ms / std::max(reps, 1);
+  QG_API_END
+}
+
 // ----------------------------------------------------- cone calculus ----
 struct ConesHandle {
   ConeTable t;

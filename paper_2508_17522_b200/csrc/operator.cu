@@ -17,8 +17,14 @@
 
 namespace qg {
 
-__device__ __forceinline__ bool lsmr_runs(const Lsmr *st, int p, int is_v_step, double &s_in, double &c_out) {
-  if (!st) { s_in = 1.0; c_out = 0.0; return true; }
+__device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in, double &c_out) {
+  const Lsmr *st = a.st;
+  const int is_v_step = a.is_v_step;
+  if (!st) {
+    s_in = a.fixed_s_in != 0.0 ? a.fixed_s_in : 1.0;
+    c_out = a.old ? a.fixed_c_out : 0.0;
+    return true;
+  }
   const Lsmr &L = st[p];
   s_in = L.s_in;
   c_out = L.c_out;
@@ -34,7 +40,7 @@ __global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
   const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
   const int p = u.prob;
   double s_in, c_out;
-  if (!lsmr_runs(a.st, p, a.is_v_step, s_in, c_out)) return;  // CTA-uniform
+  if (!lsmr_runs(a, p, s_in, c_out)) return;  // CTA-uniform
   const Embed E = M.emb[p];
   const double *inX = a.in, *inY = a.in + M.NX;
   const double wN = a.in[M.NX + M.NY + p];

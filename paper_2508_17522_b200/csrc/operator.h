@@ -20,6 +20,7 @@ struct StepArgs {
   const Lsmr *st;      // per-problem coefficients / run flags; null = (1, 0), all run
   int is_v_step;
   double *part;
+  double fixed_s_in = 0.0, fixed_c_out = 0.0;  // used when st == null (0 -> 1, 0)
 };
 
 struct FinArgs {

@@ -95,3 +95,38 @@ def product_block(tag):
     if kind in ("exp", "dexp"):
         return qg.ConeBlock(kind)
     return qg.ConeBlock(kind, dim=5)
+
+
+def synth_instance(cfg, seed=0, **kw):
+    """A synthetic instance (paper_2508_17522_b200.synth) as both oracle and
+    product objects: returns (oracle tuple, product tuple) of
+    (theta, sol, perturbation, delta)."""
+    import paper_2508_17522_b200 as qg
+    from paper_2508_17522_b200 import synth
+
+    if isinstance(cfg, tuple):
+        bt = synth.custom(*cfg, seed=seed, **kw)
+    else:
+        bt = synth.generate(cfg, seed=seed, **kw)
+    dirs = synth.directions(bt, seed=seed + 1)
+    o = synth.problem_objects(bt, 0, None)
+    n, m = o["n"], o["m"]
+    xo, yo, po, ao = o["slices"]
+    dPv, dAv = dirs.dP[po:po + o["P"][1].size], dirs.dA[ao:ao + o["A"][1].size]
+    dq, db = dirs.dq[xo:xo + n], dirs.db[yo:yo + m]
+    dx, dy, ds = dirs.dx[xo:xo + n], dirs.dy[yo:yo + m], dirs.ds[yo:yo + m]
+    P, A = Q.Csc(n, n, *o["P"]), Q.Csc(m, n, *o["A"])
+    oblocks = [C.block(k, dim=dm, order=od, alpha=al) for (k, dm, od, al) in o["blocks"]]
+    ora = (Q.Problem(P, A, o["q"], o["b"], oblocks), Q.Sol(o["x"], o["y"], o["s"]),
+           Q.Pert(Q.Csc(n, n, P.col_ptr, P.row_idx, dPv), Q.Csc(m, n, A.col_ptr, A.row_idx, dAv), dq, db),
+           Q.Delta(dx, dy, ds))
+    pblocks = []
+    for k, dm, od, al in o["blocks"]:
+        pblocks.append(qg.ConeBlock(k, dim=dm) if k in ("zero", "nonneg", "soc") else
+                       qg.ConeBlock(k, order=od) if k == "psd" else
+                       qg.ConeBlock(k, alpha=al) if k in ("pow", "dpow") else qg.ConeBlock(k))
+    Pm, Am = qg.CscMatrix(n, n, *o["P"]), qg.CscMatrix(m, n, *o["A"])
+    theta = qg.ProblemData(Pm, Am, o["q"], o["b"], qg.ConeSpec(pblocks))
+    prod = (theta, qg.Solution(o["x"], o["y"], o["s"]),
+            qg.DataPerturbation(Pm.with_values(dPv), Am.with_values(dAv), dq, db), qg.SolutionDelta(dx, dy, ds))
+    return ora, prod

@@ -131,7 +131,7 @@ def golden_file(kind):
     assert dg.iterations == d["jvp_its"]
     rng = np.random.default_rng(KCODE[kind] + 100)
     d.update(operator_probes(theta, sol, rng))
-    d.update(run_fixed(theta, sol, dtheta, delta, 5))
+    d.update(run_fixed(theta, sol, dtheta, delta, 3))
     d.update(run_tol(theta, sol, dtheta, delta, 1e-14, "t14"))
     d.update(kkt=np.array([v for k, v in sm.check_solution(theta, sol).as_dict().items()
                            if k not in ("tol", "ok")]))
@@ -255,7 +255,7 @@ def recipe(name):
     d.update(csc_arrays("dA", dtheta.dA))
     d.update(dq=dtheta.dq, db=dtheta.db, dx=delta.dx, dy=delta.dy, ds=delta.ds)
     d.update(run_tol(theta, sol, dtheta, delta, 1e-14, "t14"))
-    d.update(run_fixed(theta, sol, dtheta, delta, 5))
+    d.update(run_fixed(theta, sol, dtheta, delta, 3))
     d.update(operator_probes(theta, sol, np.random.default_rng(3)))
     np.savez_compressed(OUT / f"{name}.npz", **d)
 
