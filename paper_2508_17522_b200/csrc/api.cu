@@ -7,6 +7,7 @@
 // The loop runs in CUDA graphs of 4/16/64 iterations; every kernel reads a
 // per-problem active flag so converged problems cost no memory traffic.
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <map>
