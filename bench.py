@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: jvp+vjp evaluations per second of the QCP solution-map
+derivative (BASELINE.json metric) on B200, beside the CPU reference path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5a] [--impl ours|reference]
+
+One *step* = one evaluation of the whole workload: prepare the batch
+(``QCPBatch``: CSC->CSR transposes, Pi_K*(z), D Pi preparation), then one
+jvp and one vjp of every problem, LSMR at a fixed cap of K=100 iterations
+(atol=btol=0) -- the matched-work protocol of BASELINE.md.  ``value`` is
+evals/s with inputs resident in HBM; ``e2e`` is the same through the
+host-buffer API (H2D of the problem data and directions, D2H of all
+outputs inside the timed region).
+
+Default workload (``--config c5a``): BASELINE configs[4], a batch of 4096
+independent QCPs (n=1000, m=1500 = nonneg(500) + 100 x SOC(10), nnz(A) =
+1.5e4 each), sharded over the ranks (strong scaling of a fixed batch).
+Single-problem configs (c1..c4, c5b) run as replicas at N > 1.
+
+Multi-GPU: launched by torch.distributed.run, one rank per GPU; device
+timing max-reduced over ranks (NCCL only for that and the barrier -- the
+batch path has no data-path collective).
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c1": "n=100, m=150, zero(30)+nonneg(120), nnz(A)~1.6e3 (recipe-conditioned, diagonal P)",
+    "c2": "n=2000, m=4000, 500 x SOC(8), nnz(A)~1e5, P = I + sparse Gram",
+    "c3": "n=20000, m=40002, 6667 x exp + 6667 x pow(0.5), nnz(A)~1e6, P = I + sparse Gram",
+    "c4": "n=20000, m=280336, 512 x PSD(32) + nonneg(10000), nnz(A)~2e6, P = I + sparse Gram",
+    "c5a": "batch of 4096 QCPs, each n=1000, m=1500 = nonneg(500) + 100 x SOC(10), nnz(A)=1.5e4, diagonal P",
+    "c5b": "LASSO canonical form, n=m=20000, nnz(A)~5.0e7 (dense 10000 x 5000 features)",
+}
+BATCH = {"c5a": 4096}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5a", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lsmr-iters", type=int, default=100)
+    ap.add_argument("--batch", type=int, default=None, help="override the c5a batch size")
+    ap.add_argument("--cpu-sample", type=int, default=None, help="problems in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------ distributed --
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def init_dist(world, local, backend):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
+    return dist if world > 1 else None
+
+
+def max_over_ranks(dist, value, device=None):
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(dist, value, device=None):
+    if dist is None:
+        return value
+    import torch
+
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# -------------------------------------------------------------- workload --
+def build_workload(cfg, rank, world, batch_override=None):
+    """This rank's share of the workload (synthetic, seeded per rank)."""
+    from paper_2508_17522_b200 import synth
+
+    if cfg in BATCH:
+        total = batch_override or BATCH[cfg]
+        lo, hi = rank * total // world, (rank + 1) * total // world
+        bt = synth.generate(cfg, seed=1000 + rank, batch=hi - lo)
+        return bt, synth.directions(bt, seed=2000 + rank), total, hi - lo, "strong"
+    bt = synth.generate(cfg, seed=1000 + rank)
+    return bt, synth.directions(bt, seed=2000 + rank), world, 1, "weak"
+
+
+def batch_bytes(bt):
+    keys = ("P_colptr", "P_rowidx", "P_vals", "A_colptr", "A_rowidx", "A_vals", "q", "b", "x", "y", "s")
+    return {k: getattr(bt, k) for k in keys}
+
+
+def alg_bytes(bt):
+    """Algorithmic bytes per launch of the two fused operator kernels
+    (DESIGN.md 'Roofline'): every stored entry read once (8 B value + 4 B
+    index), row pointers once, each vector stream once, D Pi parameters
+    twice in the F' step."""
+    NX, NY = sum(bt.n), sum(bt.m)
+    nnzP, nnzA = int(bt.P_vals.size), int(bt.A_vals.size)
+    mats = 12 * (nnzP + 2 * nnzA) + 4 * (2 * NX + NY)
+    vec = 40 * (NX + NY)
+    nsoc = ntri = 0
+    psd = 0
+    for blocks in bt.blocks:
+        for (k, d, o, a) in blocks:
+            if k == "soc":
+                nsoc += 1
+            elif k == "psd":
+                psd += 16 * o * o
+            elif k in ("exp", "dexp", "pow", "dpow"):
+                ntri += 1
+    s_dpi = 8 * NY + 12 * nsoc + 76 * ntri + psd
+    return {"F": mats + vec, "FT": mats + vec + 8 * NY + 2 * s_dpi}
+
+
+# ---------------------------------------------------------------- clocks --
+class Clocks:
+    def __init__(self, device_index):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{device_index}.csv")
+        self.idx = device_index
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+            self.f.close()
+
+    def summary(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def flush_l2(buf):
+    buf.add_(1.0)
+
+
+# ------------------------------------------------------------- our arm ----
+def run_ours(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    dist = init_dist(world, local, "nccl")
+    dev = torch.device("cuda", local)
+    from paper_2508_17522_b200 import _native as N
+    from paper_2508_17522_b200 import QCPBatch
+
+    bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch)
+    K = args.lsmr_iters
+    kw = dict(atol=0.0, btol=0.0, max_iter=K)
+    blocks = [[_blk(b) for b in bl] for bl in bt.blocks]
+    host = batch_bytes(bt)
+    dev_in = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in host.items()}
+    ddir = {k: torch.from_numpy(np.ascontiguousarray(getattr(dirs, k))).to(dev)
+            for k in ("dP", "dA", "dq", "db", "dx", "dy", "ds")}
+    sizes = (bt.n, bt.m, bt.P_nnz, bt.A_nnz, blocks)
+    flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)
+
+    def step_device():
+        b = QCPBatch.from_device(*sizes, dev_in)
+        b.jvp_device(ddir["dP"], ddir["dA"], ddir["dq"], ddir["db"], **kw)
+        b.vjp_device(ddir["dx"], ddir["dy"], ddir["ds"], **kw)
+        return b
+
+    def timed(fn, steps):
+        total = 0.0
+        for _ in range(steps):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            total += e0.elapsed_time(e1)
+        return total
+
+    for _ in range(args.warmup):
+        step_device()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = N.kernel_launches()
+    with Clocks(local) as clk:
+        ms = timed(step_device, args.steps)
+    launches = (N.kernel_launches() - l0) // max(args.steps, 1)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = max_over_ranks(dist, ms, dev)
+    ms_per_step = ms / args.steps
+    value = units_total / (ms_per_step / 1e3)
+
+    # end to end through the host-buffer API: H2D of data + directions, D2H of outputs
+    e2e = None
+    if not args.no_e2e:
+        pin = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in host.items()}
+        pdir = {k: torch.from_numpy(np.ascontiguousarray(getattr(dirs, k))).pin_memory()
+                for k in ("dP", "dA", "dq", "db", "dx", "dy", "ds")}
+        outs = {}
+
+        def step_host():
+            b = QCPBatch.from_host(*sizes, pin)
+            outs["j"] = b.jvp_host(pdir["dP"], pdir["dA"], pdir["dq"], pdir["db"], **kw)
+            outs["v"] = b.vjp_host(pdir["dx"], pdir["dy"], pdir["ds"], **kw)
+            b.close()
+
+        step_host()
+        if dist:
+            dist.barrier()
+        ems = max_over_ranks(dist, timed(step_host, max(1, min(args.steps, 3))), dev) / max(1, min(args.steps, 3))
+        h2d = sum(v.numel() * v.element_size() for v in pin.values()) + sum(
+            v.numel() * v.element_size() for v in pdir.values())
+        d2h = 8 * (sum(bt.n) * 2 + sum(bt.m) * 3 + bt.P_vals.size + bt.A_vals.size)
+        e2e = {"value": units_total / (ems / 1e3), "unit": "evals/s", "h2d_bytes_per_step": int(h2d * world),
+               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": ems}
+
+    # roofline of the fused kernels (CUDA events inside the library, same stream)
+    b = step_device()
+    ab = alg_bytes(bt)
+    t_ft = b.time_kernel(1, reps=20)
+    t_f = b.time_kernel(0, reps=20)
+    peaks = _peaks()
+    ach = ab["FT"] / (t_ft / 1e3) / 1e9
+    roof = {"kernel": "k_step<FT> (CSR SpMV A,A',P + D Pi x2 epilogue)", "bound": "hbm",
+            "achieved": round(ach, 1), "peak": peaks[0], "peak_source": peaks[1], "unit": "GB/s",
+            "frac": round(ach / peaks[0], 4), "traffic": _traffic(args.config, ab["FT"]),
+            "alg_bytes_per_launch": ab["FT"], "launch_ms": round(t_ft, 4),
+            "f_step": {"achieved": round(ab["F"] / (t_f / 1e3) / 1e9, 1), "launch_ms": round(t_f, 4),
+                       "alg_bytes_per_launch": ab["F"]}}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(bt, dirs, K, args, scaling)
+    if rank == 0:
+        line = {
+            "metric": "jvp+vjp evals/s", "value": round(value, 3), "unit": "evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+            "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (KKT-reverse instances, SURVEY §8(d) recipe; random directions)",
+            "config": {"workload": f"{args.config}: {CONFIGS[args.config]}", "evals_per_step": units_total,
+                       "per_rank_problems": units_here,
+                       "lsmr": f"fixed cap K={K} (atol=btol=0) for jvp and vjp; step includes batch preparation",
+                       "l2": "256 MiB L2 flush between timed steps (excluded from timing)",
+                       "parallelism": f"{'batch shards' if scaling == 'strong' else 'replicas'} x{world}"},
+            "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
+            "clocks": clk.summary(), "lsmr_iterations_per_s": round(value * 2 * K, 1),
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _blk(b):
+    from paper_2508_17522_b200.cones import ConeBlock
+
+    k, d, o, a = b
+    if k == "psd":
+        return ConeBlock(k, order=o)
+    if k in ("pow", "dpow"):
+        return ConeBlock(k, alpha=a)
+    if k in ("exp", "dexp"):
+        return ConeBlock(k)
+    return ConeBlock(k, dim=d)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def _traffic(cfg, alg):
+    """dram bytes per launch of the same kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(cfg)
+    except (OSError, ValueError):
+        return None
+
+
+# --------------------------------------------------------- CPU reference --
+def cpu_sample_size(args, scaling, cores):
+    if args.cpu_sample:
+        return args.cpu_sample
+    return cores if scaling == "strong" else 1
+
+
+def cpu_baseline(bt, dirs, K, args, scaling):
+    """The oracle (the reference algorithm restated) on the host cores."""
+    from oracle import cpu_bench
+
+    cores = cpu_bench.host_cores()
+    nprob = bt.B
+    sample = min(cpu_sample_size(args, scaling, cores), nprob)
+    workers = min(cores, sample)
+    secs = cpu_bench.time_sample(bt, dirs, K, range(sample), workers)
+    return {"value": round(sample / secs, 4), "unit": "evals/s", "cores": workers, "kind": "port",
+            "sample": f"{sample} of {nprob} problems of this rank's workload, jvp+vjp at K={K}, "
+                      f"{workers} processes x 1 thread ({cpu_bench.cpu_model()})",
+            "seconds": round(secs, 2)}
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return  # rank 0 alone times the CPU reference
+    from oracle import cpu_bench
+
+    bt, dirs, units_total, units_here, scaling = build_workload(args.config, 0, 1, args.batch)
+    K = args.lsmr_iters
+    cores = cpu_bench.host_cores()
+    sample = min(cpu_sample_size(args, scaling, cores), bt.B)
+    workers = min(cores, sample)
+    for _ in range(args.warmup):
+        cpu_bench.time_sample(bt, dirs, K, range(sample), workers)
+    secs = [cpu_bench.time_sample(bt, dirs, K, range(sample), workers) for _ in range(args.steps)]
+    value = sample / (sum(secs) / len(secs))
+    line = {
+        "impl": "reference", "metric": "jvp+vjp evals/s", "value": round(value, 4), "unit": "evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(secs) / len(secs), 3), "higher_is_better": True, "scaling": scaling,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator and seeds as the GPU arm)",
+        "config": {"workload": f"{args.config}: {CONFIGS[args.config]}",
+                   "lsmr": f"fixed cap K={K} (atol=btol=0)", "sample_problems_per_step": sample},
+        "cpu_baseline": {"value": round(value, 4), "unit": "evals/s", "cores": workers, "kind": "port",
+                         "sample": f"{sample} problems per step, {workers} processes x 1 thread "
+                                   f"({cpu_bench.cpu_model()})"},
+        "e2e": {"value": round(value, 4), "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

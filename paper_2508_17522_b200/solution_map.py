@@ -179,6 +179,40 @@ class QCPBatch:
         self._sol_dev = (tensors["x"], tensors["y"], tensors["s"])
         return self
 
+    @classmethod
+    def from_host(cls, n, m, P_nnz, A_nnz, blocks, arrays):
+        """Create from concatenated HOST arrays (NumPy or pinned torch CPU
+        tensors, keys as in ``qg_batch_desc``): the host-buffer boundary."""
+        import torch
+
+        f64, i64 = torch.float64, torch.int64
+        t = {k: N.to_dev(v, i64 if k.endswith(("colptr", "rowidx")) else f64) for k, v in arrays.items()}
+        return cls.from_device(n, m, P_nnz, A_nnz, blocks, t)
+
+    def jvp_host(self, dP, dA, dq, db, **kw):
+        """jvp from concatenated host arrays on the patterns of P / A; returns
+        host (dx, dy, ds) and per-problem Diagnostics."""
+        import torch
+
+        d = [N.to_dev(a, torch.float64) for a in (dP, dA, dq, db)]
+        dx, dy, ds, diags = self.jvp_device(*d, **kw)
+        return dx.cpu().numpy(), dy.cpu().numpy(), ds.cpu().numpy(), [_diag(g) for g in diags]
+
+    def vjp_host(self, dx, dy, ds, **kw):
+        import torch
+
+        d = [N.to_dev(a, torch.float64) for a in (dx, dy, ds)]
+        dP, dA, dq, db, diags = self.vjp_device(*d, **kw)
+        return (dP.cpu().numpy(), dA.cpu().numpy(), dq.cpu().numpy(), db.cpu().numpy(),
+                [_diag(g) for g in diags])
+
+    def time_kernel(self, which, reps=20):
+        """Mean device ms per launch of a hot kernel (0: F step, 1: F' step,
+        2: LSMR update), CUDA events on the current stream."""
+        ms = N.c_dbl()
+        N.check(N.lib().qg_time_kernel(self._h, int(which), int(reps), N.ctypes.byref(ms), N.stream_ptr()))
+        return float(ms.value)
+
     def _create(self, n, m, P_nnz, A_nnz, blocks, t):
         lib = N.lib()
         self.B = len(n)
