@@ -211,7 +211,7 @@ def run_ours(args):
     bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch)
     K = args.lsmr_iters
     kw = dict(atol=0.0, btol=0.0, max_iter=K)
-    blocks = [[_blk(b) for b in bl] for bl in bt.blocks]
+    blocks = bt.blocks  # (kind, dim, order, alpha) per block; shared list objects convert once
     host = batch_bytes(bt)
     dev_in = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in host.items()}
     ddir = {k: torch.from_numpy(np.ascontiguousarray(getattr(dirs, k))).to(dev)

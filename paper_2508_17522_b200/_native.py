@@ -181,6 +181,40 @@ def cone_array(blocks):
     return arr
 
 
+CONE_DTYPE = np.dtype([("kind", np.int32), ("dim", np.int32), ("order", np.int32), ("_pad", np.int32),
+                       ("alpha", np.float64)])
+
+
+def cone_struct(blocks):
+    """Structured array in qg_cone_block layout from ConeBlock objects or
+    (kind, dim, order, alpha) tuples."""
+    out = np.zeros(len(blocks), dtype=CONE_DTYPE)
+    for i, b in enumerate(blocks):
+        if isinstance(b, tuple):
+            k, d, o, a = b
+        else:
+            k, d, o, a = b.kind, b.dim, b.order, b.alpha
+        out[i] = (KIND_CODE[k], int(d), int(o or 0), 0, float(a or 0.0))
+    return out
+
+
+def cone_table(per_problem):
+    """Concatenated cone table for a batch; lists shared between problems
+    (the same list object) are converted once."""
+    cache, parts = {}, []
+    for bl in per_problem:
+        arr = cache.get(id(bl))
+        if arr is None:
+            arr = cache[id(bl)] = cone_struct(bl)
+        parts.append(arr)
+    flat = np.concatenate(parts) if parts else np.zeros(0, dtype=CONE_DTYPE)
+    return np.ascontiguousarray(flat), np.array([len(b) for b in per_problem], dtype=np.int64)
+
+
+def as_i64_ptr(arr):
+    return arr.ctypes.data_as(P_i64)
+
+
 def i64_array(values):
     arr = (c_i64 * max(len(values), 1))()
     for i, v in enumerate(values):

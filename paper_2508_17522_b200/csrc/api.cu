@@ -7,7 +7,10 @@
 // The loop runs in CUDA graphs of 4/16/64 iterations; every kernel reads a
 // per-problem active flag so converged problems cost no memory traffic.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -28,6 +31,24 @@ int fail(int code, const std::string &msg) {
 }
 void count_launch(int n) { g_launches += n; }
 
+cudaStream_t &alloc_stream() {
+  static thread_local cudaStream_t s = nullptr;
+  return s;
+}
+
+void init_pool() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
+}
+
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
@@ -46,6 +67,8 @@ static std::mutex g_graph_mu;
 
 Handle::~Handle() {
   P.release(); Pc.release(); A.release(); AT.release();
+  sP.release(); sAT.release(); sA.release();
+  dev_free(x_rowof); dev_free(y_rowof);
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   ws.release();
@@ -66,7 +89,22 @@ static int pick_group(int64_t nnz, int64_t rows) {
 }
 
 // ------------------------------------------------------------ create ----
+struct Tracer {
+  bool on;
+  cudaStream_t st;
+  std::chrono::steady_clock::time_point t0;
+  explicit Tracer(cudaStream_t s) : on(std::getenv("QG_TRACE") != nullptr), st(s), t0(std::chrono::steady_clock::now()) {}
+  void operator()(const char *what) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[qg] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
+  Tracer trace(st);
   const int B = (int)d.nprob;
   if (B <= 0) throw Error{QG_ERR_VALIDATION, "batch must hold at least one problem"};
   H.B = B;
@@ -92,11 +130,13 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   // sparse structures
   CscBatch cp{d.P_colptr, d.P_rowidx, d.P_vals, H.n, H.n, H.nnzP};
   csc_to_csr(cp, H.P, &H.Pc, true, st);
+  trace("transpose P");
   CscBatch ca{d.A_colptr, d.A_rowidx, d.A_vals, H.n, H.m, H.nnzA};
   csc_to_csr(ca, H.A, &H.AT, true, st);
   H.AT.val = dev_alloc<double>(H.noffA[B]);
   if (H.noffA[B])
     QG_CUDA(cudaMemcpyAsync(H.AT.val, d.A_vals, sizeof(double) * H.noffA[B], cudaMemcpyDeviceToDevice, st));
+  trace("transpose A");
 
   // row-length statistics for the group sizes and unit partition
   std::vector<int32_t> rpP(H.NX + 1), rpAT(H.NX + 1), rpA(H.NY + 1);
@@ -104,6 +144,7 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   QG_CUDA(cudaMemcpyAsync(rpAT.data(), H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaMemcpyAsync(rpA.data(), H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
+  trace("rowptr D2H");
   const int64_t nnzX = (int64_t)rpP[H.NX] + rpAT[H.NX], nnzY = rpA[H.NY];
   H.gx = pick_group(nnzX, H.NX);
   H.gy = pick_group(nnzY, H.NY);
@@ -141,7 +182,11 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     per[p].assign(d.blocks + bi, d.blocks + bi + d.nblocks[p]);
     bi += d.nblocks[p];
   }
+  trace("x units");
   H.cones.build(per, H.yoff, target_rows_y, st);
+  trace("cone table");
+  build_sell(H, rpP, rpAT, rpA, st);
+  trace("sell layout");
   H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
   H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xunit_ptr, H.xunit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
@@ -171,14 +216,17 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
   QG_CUDA(cudaMallocHost(&W.h_nactive, sizeof(int)));
+  trace("workspace");
 
   // embedding: z = (x, y - s, 1); Pi z; D Pi prep; P xbar, xbar'P xbar
   double *zmid = H.cones.d_zmid;
   launch_embed_prep(H, d.x, d.y, d.s, zmid, st);
   H.cones.prepare(zmid, H.ybar, 1, true, st);
   H.cones.check_errors(st);
+  trace("cone prep");
   Mats M = make_mats(H);
   launch_embed_consts(H, M, W.part, st);
+  trace("embedding consts");
 }
 
 }  // namespace qg
@@ -335,7 +383,10 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
 
 using namespace qg;
 
-#define QG_API_BEGIN try {
+#define QG_API_BEGIN_NS try {
+#define QG_API_BEGIN \
+  try {              \
+    qg::StreamScope _scope((cudaStream_t)stream);
 #define QG_API_END                                                     \
   return QG_OK;                                                        \
   }                                                                    \
@@ -365,13 +416,13 @@ int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream) {
 }
 
 int qg_destroy(qg_handle *h) {
-  QG_API_BEGIN
+  QG_API_BEGIN_NS
   delete reinterpret_cast<Handle *>(h);
   QG_API_END
 }
 
 int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_t *total_m) {
-  QG_API_BEGIN
+  QG_API_BEGIN_NS
   const Handle *H = reinterpret_cast<const Handle *>(h);
   *nprob = H->B;
   *total_n = H->NX;
@@ -600,7 +651,7 @@ int qg_cones_create(qg_cones **out, const qg_cone_block *blocks, int64_t nblocks
 }
 
 int qg_cones_destroy(qg_cones *c) {
-  QG_API_BEGIN
+  QG_API_BEGIN_NS
   delete reinterpret_cast<ConesHandle *>(c);
   QG_API_END
 }

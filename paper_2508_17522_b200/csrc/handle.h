@@ -44,6 +44,16 @@ struct DevCsr {
   void release();
 };
 
+struct SellMat {
+  int64_t *off = nullptr;
+  int32_t *w = nullptr;
+  int32_t *col = nullptr;
+  double *val = nullptr;
+  int64_t entries = 0;
+  SellView view() const { return SellView{off, w, col, val}; }
+  void release();
+};
+
 struct Workspace {
   double *u = nullptr, *v = nullptr, *h = nullptr, *hb = nullptr, *x = nullptr;  // EVec
   double *dpu = nullptr, *dpv = nullptr, *tY = nullptr, *tY2 = nullptr;          // Y
@@ -63,6 +73,10 @@ struct Handle {
   DevCsr A;    // CSR of A
   DevCsr AT;   // CSC of A read as CSR of A' (rows = columns of A, cols = global Y)
   ConeTable cones;
+  SellMat sP, sAT, sA;          // SELL copies of P, A' (X rows) and A (Y rows)
+  int32_t *x_rowof = nullptr;   // [32 * x slices] row of each slice lane (-1 = padding)
+  int32_t *y_rowof = nullptr;
+  int64_t nslice_x = 0, nslice_y = 0;
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;
@@ -89,5 +103,10 @@ struct CscBatch {
   std::vector<int64_t> ncols, nrows, nnz;  // per problem
 };
 void csc_to_csr(const CscBatch &in, DevCsr &out, DevCsr *csc_as_rows, bool keep_perm, cudaStream_t st);
+
+// SELL copies of P, A' (X units) and A (Y units); sets unit modes / slices
+// (sell.cu).  rp* are host copies of the CSR row pointers.
+void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
+                const std::vector<int32_t> &rpA, cudaStream_t st);
 
 }  // namespace qg

@@ -32,6 +32,34 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 }
 
 // ------------------------------------------------------------- op steps --
+// Iterate the rows of a unit: MODE_SELL -> one thread per row over the unit's
+// SELL slices; MODE_LONG -> a group of G lanes per CSR row.  `row(r, s1, s2)`
+// receives the row sums of the one or two matrices (second may be unused).
+template <class RowFn>
+__device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
+                                         const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
+                                         const double *v1, const int32_t *rp2, const int32_t *c2,
+                                         const double *v2, const double *x1, const double *x2, RowFn row) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (u.mode == MODE_SELL) {
+    for (int s = u.s0 + warp; s < u.s1; s += kWarps) {
+      const int r = rowof[(int64_t)s * 32 + lane];
+      const double s1 = sell_dot(S1, s, lane, x1);
+      const double s2 = S2 ? sell_dot(*S2, s, lane, x2) : 0.0;
+      if (r >= 0) row(r, s1, s2);
+    }
+  } else {
+    const int G = 32;
+    for (int r = u.row0 + warp; r < u.row1; r += kWarps) {
+      double s1 = row_dot(rp1, c1, v1, x1, r, lane, G);
+      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, G) : 0.0;
+      s1 = gsum(s1, G);
+      s2 = gsum(s2, G);
+      if (lane == 0) row(r, s1, s2);
+    }
+  }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
   extern __shared__ double sm[];
@@ -45,68 +73,46 @@ __global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
   const double *inX = a.in, *inY = a.in + M.NX;
   const double wN = a.in[M.NX + M.NY + p];
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   if (isx) {
-    const int G = M.gx, lg = lane & (G - 1), gpw = 32 / G;
-    for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
-      const int r = base + lane / G;
-      const bool valid = r < u.row1;
-      double s1 = 0.0, s2 = 0.0;
-      if (valid) {
-        s1 = row_dot(M.P_rp, M.P_col, M.P_val, inX, r, lg, G);
-        s2 = row_dot(M.AT_rp, M.AT_col, M.AT_val, KIND == STEP_F ? a.dpin : inY, r, lg, G);
-      }
-      s1 = gsum(s1, G);
-      s2 = gsum(s2, G);
-      if (valid && lg == 0) {
-        const double w = inX[r];
-        double res;
-        if (KIND == STEP_F) {
-          // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
-          const double o1 = (s1 + s2) + wN * M.q[r];
-          res = ((o1 - w) + w) / E.zN;
-          acc[0] += M.Pxbar[r] * w;
-        } else {
-          // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
-          const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
-          res = ((g - w) + w) / E.zN;
-        }
-        acc[1] += M.q[r] * w;
-        const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
-        a.out[r] = o;
-        acc[2] += o * o;
-      }
-    }
+    const double *x2 = KIND == STEP_F ? a.dpin : inY;
+    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
+             [&](int r, double s1, double s2) {
+               const double w = inX[r];
+               double res;
+               if (KIND == STEP_F) {
+                 // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
+                 const double o1 = (s1 + s2) + wN * M.q[r];
+                 res = ((o1 - w) + w) / E.zN;
+                 acc[0] += M.Pxbar[r] * w;
+               } else {
+                 // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
+                 const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
+                 res = ((g - w) + w) / E.zN;
+               }
+               acc[1] += M.q[r] * w;
+               const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
+               a.out[r] = o;
+               acc[2] += o * o;
+             });
   } else {
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
-    const int G = M.gy, lg = lane & (G - 1), gpw = 32 / G;
     if (KIND == STEP_F) {
-      for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
-        const int r = base + lane / G;
-        const bool valid = r < u.row1;
-        double s = valid ? row_dot(M.A_rp, M.A_col, M.A_val, inX, r, lg, G) : 0.0;
-        s = gsum(s, G);
-        if (valid && lg == 0) {
-          // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
-          const double o2 = (-s) + wN * M.b[r];
-          const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
-          const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
-          outY[r] = o;
-          acc[0] += M.b[r] * a.dpin[r];
-          acc[2] += o * o;
-        }
-      }
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+               [&](int r, double s, double) {
+                 // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
+                 const double o2 = (-s) + wN * M.b[r];
+                 const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+                 const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+                 outY[r] = o;
+                 acc[0] += M.b[r] * a.dpin[r];
+                 acc[2] += o * o;
+               });
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
-      for (int base = u.row0 + warp * gpw; base < u.row1; base += kWarps * gpw) {
-        const int r = base + lane / G;
-        const bool valid = r < u.row1;
-        double s = valid ? row_dot(M.A_rp, M.A_col, M.A_val, inX, r, lg, G) : 0.0;
-        s = gsum(s, G);
-        if (valid && lg == 0) a.tY[r] = (s - wN * M.b[r]) - inY[r];
-      }
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+               [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
       __syncthreads();
       // r = D Pi t  (blockwise, in the unit)
       dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
@@ -425,6 +431,8 @@ Mats make_mats(const Handle &H) {
   M.NX = H.NX; M.NY = H.NY;
   M.gx = H.gx; M.gy = H.gy;
   M.dpi = H.cones.view();
+  M.sP = H.sP.view(); M.sAT = H.sAT.view(); M.sA = H.sA.view();
+  M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
   return M;
 }
 

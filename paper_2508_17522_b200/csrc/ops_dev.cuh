@@ -18,7 +18,22 @@ struct Mats {
   int64_t NX, NY;
   int gx, gy;
   DpiView dpi;
+  SellView sP, sAT, sA;                 // SELL copies (MODE_SELL units)
+  const int32_t *x_rowof, *y_rowof;     // lane -> row per slice (-1 = padding)
 };
+
+// Row sum of one SELL slice lane: sum_k val * vec[col] in storage order.
+__device__ __forceinline__ double sell_dot(const SellView &S, int64_t s, int lane, const double *vec) {
+  const int64_t o = S.off[s] + lane;
+  const int w = S.w[s];
+  double acc = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < w; ++k) {
+    const int64_t p = o + 32LL * k;
+    acc += __ldcs(S.val + p) * vec[__ldcs(S.col + p)];
+  }
+  return acc;
+}
 
 // Group-of-G sum inside a warp (G power of two, runtime).
 __device__ __forceinline__ double gsum(double v, int G) {

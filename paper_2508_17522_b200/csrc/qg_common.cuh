@@ -85,6 +85,22 @@ struct Unit {
   int32_t row0, row1;
   int32_t blk0, blk1;
   int32_t cls;
+  int32_t mode;    // MODE_SELL: thread-per-row over SELL slices [s0, s1); MODE_LONG: warp-per-row CSR
+  int32_t s0, s1;
+  int32_t pad_;
+};
+
+enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1 };
+
+// SELL-C-sigma storage (C = 32 = warp width, sigma = the work unit): the rows
+// of a unit are sorted by length (descending) and cut into slices of 32; in
+// slice s entry k of lane l sits at off[s] + 32 k + l, so a warp reads 32
+// consecutive values per step (fully coalesced) and each thread owns one row.
+struct SellView {
+  const int64_t *off;   // [nslices] first entry of the slice
+  const int32_t *w;     // [nslices] slice width (longest row)
+  const int32_t *col;   // padded entries: col 0, val 0
+  const double *val;
 };
 
 struct Csr {
@@ -131,16 +147,30 @@ __device__ __forceinline__ void cta_sum_slots(double (&v)[kSlots], double *smem_
   __syncthreads();
 }
 
+// Stream-ordered allocation from the device's default memory pool (kept
+// resident between handles: no cudaMalloc/cudaFree synchronisation on the
+// per-batch path).  The stream is the calling API entry's stream.
+cudaStream_t &alloc_stream();
+void init_pool();
+
 template <class T>
 inline T *dev_alloc(size_t count) {
   if (count == 0) count = 1;
+  init_pool();
   T *p = nullptr;
-  QG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  QG_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), alloc_stream()));
   return p;
 }
 
 inline void dev_free(void *p) {
-  if (p) cudaFree(p);
+  if (p) cudaFreeAsync(p, alloc_stream());
 }
+
+// Sets the allocation stream for the duration of an API call.
+struct StreamScope {
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(alloc_stream()) { alloc_stream() = s; }
+  ~StreamScope() { alloc_stream() = prev; }
+};
 
 }  // namespace qg

@@ -224,14 +224,15 @@ class QCPBatch:
         self.yoff = np.concatenate([[0], np.cumsum(self.m)]).astype(np.int64)
         self.poff = np.concatenate([[0], np.cumsum(self.P_nnz)]).astype(np.int64)
         self.aoff = np.concatenate([[0], np.cumsum(self.A_nnz)]).astype(np.int64)
-        flat = [b for bl in blocks for b in bl]
-        keep = dict(n=N.i64_array(self.n), m=N.i64_array(self.m), pn=N.i64_array(self.P_nnz),
-                    an=N.i64_array(self.A_nnz), nb=N.i64_array([len(b) for b in blocks]),
-                    blk=N.cone_array(flat))
+        table, counts = N.cone_table(blocks)
+        keep = dict(n=np.asarray(self.n, dtype=np.int64), m=np.asarray(self.m, dtype=np.int64),
+                    pn=np.asarray(self.P_nnz, dtype=np.int64), an=np.asarray(self.A_nnz, dtype=np.int64),
+                    nb=counts, blk=table)
         d = N.BatchDesc()
         d.nprob = self.B
-        d.n, d.m, d.P_nnz, d.A_nnz, d.nblocks = keep["n"], keep["m"], keep["pn"], keep["an"], keep["nb"]
-        d.blocks = keep["blk"]
+        d.n, d.m = N.as_i64_ptr(keep["n"]), N.as_i64_ptr(keep["m"])
+        d.P_nnz, d.A_nnz, d.nblocks = N.as_i64_ptr(keep["pn"]), N.as_i64_ptr(keep["an"]), N.as_i64_ptr(keep["nb"])
+        d.blocks = table.ctypes.data_as(N.ctypes.POINTER(N.ConeBlockC))
         for k in ("P_colptr", "P_rowidx", "P_vals", "A_colptr", "A_rowidx", "A_vals", "q", "b", "x", "y", "s"):
             setattr(d, k, t[k].data_ptr())
         h = N.c_vp()
