@@ -11,6 +11,8 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <cstdlib>
+
 #include "handle.h"
 
 namespace qg {
@@ -138,6 +140,8 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
                    int32_t **rowof_out, cudaStream_t st) {
   std::vector<int32_t> slice_pos, slice_n;
   int64_t ns = 0;
+  int max_row = kSellMaxRow;
+  if (const char *e = std::getenv("QG_SELL_MAX_ROW")) max_row = std::atoi(e);  // A/B switch (diagnostics)
   for (auto &u : units) {
     int maxlen = 0;
     for (int r = u.row0; r < u.row1; ++r) {
@@ -145,7 +149,7 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
       if (rp2) len = std::max(len, (*rp2)[r + 1] - (*rp2)[r]);
       maxlen = std::max(maxlen, len);
     }
-    u.mode = maxlen > kSellMaxRow ? MODE_LONG : MODE_SELL;
+    u.mode = maxlen > max_row ? MODE_LONG : MODE_SELL;
     u.s0 = u.s1 = (int32_t)ns;
     if (u.mode == MODE_SELL) {
       for (int r = u.row0; r < u.row1; r += 32) {
@@ -193,9 +197,23 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
 
 void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
                 const std::vector<int32_t> &rpA, cudaStream_t st) {
+  const char *side = std::getenv("QG_SELL_SIDE");  // diagnostics: "x" or "y" only
+  const std::string keep = side ? side : "xy";
+  const char *saved = std::getenv("QG_SELL_MAX_ROW");
+  std::string saved_s = saved ? saved : "";
+  auto with_side = [&](bool on) {
+    if (on) {
+      if (saved) setenv("QG_SELL_MAX_ROW", saved_s.c_str(), 1); else unsetenv("QG_SELL_MAX_ROW");
+    } else {
+      setenv("QG_SELL_MAX_ROW", "-1", 1);
+    }
+  };
+  with_side(keep.find('x') != std::string::npos);
   H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, st);
+  with_side(keep.find('y') != std::string::npos);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
                           &H.y_rowof, st);
+  with_side(true);
 }
 
 }  // namespace qg
