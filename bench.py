@@ -104,13 +104,18 @@ def sum_over_ranks(dist, value, device=None):
 
 
 # -------------------------------------------------------------- workload --
+def shard_range(total, rank, world):
+    """Contiguous, balanced problem range of ``rank``."""
+    return rank * total // world, (rank + 1) * total // world
+
+
 def build_workload(cfg, rank, world, batch_override=None):
     """This rank's share of the workload (synthetic, seeded per rank)."""
     from paper_2508_17522_b200 import synth
 
     if cfg in BATCH:
         total = batch_override or BATCH[cfg]
-        lo, hi = rank * total // world, (rank + 1) * total // world
+        lo, hi = shard_range(total, rank, world)
         bt = synth.generate(cfg, seed=1000 + rank, batch=hi - lo)
         return bt, synth.directions(bt, seed=2000 + rank), total, hi - lo, "strong"
     bt = synth.generate(cfg, seed=1000 + rank)

@@ -56,13 +56,23 @@ void Workspace::release() {
   if (h_nactive) cudaFreeHost(h_nactive);
 }
 
+// Captured (not instantiated) LSMR graphs per handle, keyed by (jvp, iters).
 struct GraphCache {
-  std::map<std::pair<int, int>, cudaGraphExec_t> exec;
+  std::map<std::pair<int, int>, cudaGraph_t> graph;
   ~GraphCache() {
-    for (auto &kv : exec) cudaGraphExecDestroy(kv.second);
+    for (auto &kv : graph) cudaGraphDestroy(kv.second);
   }
 };
+// One executable graph per (jvp, iters) shared by all handles: switching
+// handles re-points its kernel nodes with cudaGraphExecUpdate (same topology,
+// new arguments / grid sizes) instead of re-instantiating -- a new batch per
+// training step pays one capture, not an instantiation.
+struct SharedExec {
+  cudaGraphExec_t exec = nullptr;
+  const Handle *owner = nullptr;
+};
 static std::map<const Handle *, GraphCache *> g_graphs;
+static std::map<std::pair<int, int>, SharedExec> g_exec;
 static std::mutex g_graph_mu;
 
 Handle::~Handle() {
@@ -78,6 +88,8 @@ Handle::~Handle() {
     delete it->second;
     g_graphs.erase(it);
   }
+  for (auto &kv : g_exec)
+    if (kv.second.owner == this) kv.second.owner = nullptr;  // must be re-pointed before next use
 }
 
 static int pick_group(int64_t nnz, int64_t rows) {
@@ -267,17 +279,7 @@ static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStr
   }
 }
 
-static cudaGraphExec_t get_graph(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
-  GraphCache *gc;
-  {
-    std::lock_guard<std::mutex> g(g_graph_mu);
-    auto it = g_graphs.find(&H);
-    if (it == g_graphs.end()) it = g_graphs.emplace(&H, new GraphCache()).first;
-    gc = it->second;
-  }
-  auto key = std::make_pair(jvp ? 1 : 0, iters);
-  auto it = gc->exec.find(key);
-  if (it != gc->exec.end()) return it->second;
+static cudaGraph_t capture_graph(Handle &H, const Mats &M, bool jvp, int iters) {
   cudaStream_t cs;
   QG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaGraph_t graph;
@@ -292,13 +294,33 @@ static cudaGraphExec_t get_graph(Handle &H, const Mats &M, bool jvp, int iters, 
   }
   g_launches = before;  // captured launches are counted when the graph runs
   QG_CUDA(cudaStreamEndCapture(cs, &graph));
-  cudaGraphExec_t exec;
-  QG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
-  cudaGraphDestroy(graph);
   cudaStreamDestroy(cs);
-  gc->exec[key] = exec;
-  (void)st;
-  return exec;
+  return graph;
+}
+
+// Launch `iters` LSMR iterations of handle H as one graph on `st`.
+static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
+  const auto key = std::make_pair(jvp ? 1 : 0, iters);
+  std::lock_guard<std::mutex> lock(g_graph_mu);
+  auto git = g_graphs.find(&H);
+  if (git == g_graphs.end()) git = g_graphs.emplace(&H, new GraphCache()).first;
+  GraphCache *gc = git->second;
+  auto cit = gc->graph.find(key);
+  if (cit == gc->graph.end()) cit = gc->graph.emplace(key, capture_graph(H, M, jvp, iters)).first;
+  SharedExec &se = g_exec[key];
+  if (se.exec == nullptr) {
+    QG_CUDA(cudaGraphInstantiate(&se.exec, cit->second, 0));
+  } else if (se.owner != &H) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(se.exec, cit->second, &info) != cudaSuccess) {
+      cudaGetLastError();  // clear the sticky-free update error, fall back to a fresh instantiation
+      cudaGraphExecDestroy(se.exec);
+      se.exec = nullptr;
+      QG_CUDA(cudaGraphInstantiate(&se.exec, cit->second, 0));
+    }
+  }
+  se.owner = &H;
+  QG_CUDA(cudaGraphLaunch(se.exec, st));
 }
 
 static int kernels_per_iter(const Handle &H) {
@@ -314,9 +336,10 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
     QG_CUDA(cudaStreamSynchronize(st));
     if (*W.h_nactive == 0 || done >= cap) break;
     const long long rem = cap - done;
-    const int g = rem >= 64 ? 64 : (rem >= 16 ? 16 : (rem >= 4 ? 4 : 1));
-    cudaGraphExec_t ex = get_graph(H, M, jvp, g, st);
-    QG_CUDA(cudaGraphLaunch(ex, st));
+    // 16 first (early convergence wastes little), then chunks of 64
+    const long long want = done == 0 ? std::min<long long>(rem, 16) : rem;
+    const int g = want >= 64 ? 64 : (want >= 16 ? 16 : (want >= 4 ? 4 : 1));
+    launch_iters(H, M, jvp, g, st);
     count_launch(g * kernels_per_iter(H));
     done += g;
   }

@@ -268,7 +268,7 @@ void ConeTable::build(const std::vector<std::vector<qg_cone_block>> &per_prob, c
         ++bi;
       } else {
         const int cls = (b.kind == QG_CONE_SOC) ? CLS_SOC : CLS_TRI;
-        const int64_t maxblk = (cls == CLS_SOC) ? 4 * kWarps : kThreads;
+        const int64_t maxblk = (cls == CLS_SOC) ? 16 * kWarps : kThreads;
         int64_t e = bi, rows = 0;
         while (e < bend && e - bi < maxblk) {
           const BlockInfo &c = h_blk[e];

@@ -42,11 +42,23 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
                                          const double *v2, const double *x1, const double *x2, RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
-    for (int s = u.s0 + warp; s < u.s1; s += kWarps) {
-      const int r = rowof[(int64_t)s * 32 + lane];
-      const double s1 = sell_dot(S1, s, lane, x1);
-      const double s2 = S2 ? sell_dot(*S2, s, lane, x2) : 0.0;
-      if (r >= 0) row(r, s1, s2);
+    // warps claim pairs of slices dynamically (balances uneven units)
+    __shared__ int next_slice;
+    if (threadIdx.x == 0) next_slice = u.s0;
+    __syncthreads();
+    while (true) {
+      int s = 0;
+      if (lane == 0) s = atomicAdd(&next_slice, 2);
+      s = __shfl_sync(0xffffffffu, s, 0);
+      if (s >= u.s1) break;
+      const int sb = s + 1 < u.s1 ? s + 1 : -1;
+      const int ra = rowof[(int64_t)s * 32 + lane];
+      const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
+      double a1, b1, a2 = 0.0, b2 = 0.0;
+      sell_dot2(S1, s, sb, lane, x1, a1, b1);
+      if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
+      if (ra >= 0) row(ra, a1, a2);
+      if (rb >= 0) row(rb, b1, b2);
     }
   } else {
     const int G = 32;

@@ -35,6 +35,40 @@ __device__ __forceinline__ double sell_dot(const SellView &S, int64_t s, int lan
   return acc;
 }
 
+// Two slices of one matrix at once (independent load streams -> twice the
+// memory-level parallelism per warp); slice b may be absent (sb < 0).  Each
+// lane's sums stay in storage order.
+__device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t sb, int lane, const double *vec,
+                                          double &acc_a, double &acc_b) {
+  const int64_t oa = S.off[sa] + lane;
+  const int wa = S.w[sa];
+  const int64_t ob = sb >= 0 ? S.off[sb] + lane : 0;
+  const int wb = sb >= 0 ? S.w[sb] : 0;
+  const int wm = wa < wb ? wa : wb;
+  double a = 0.0, b = 0.0;
+  int k = 0;
+#pragma unroll 4
+  for (; k < wm; ++k) {
+    const int64_t pa = oa + 32LL * k, pb = ob + 32LL * k;
+    const double va = __ldcs(S.val + pa), vb = __ldcs(S.val + pb);
+    const int ca = __ldcs(S.col + pa), cb = __ldcs(S.col + pb);
+    a += va * vec[ca];
+    b += vb * vec[cb];
+  }
+#pragma unroll 4
+  for (int j = k; j < wa; ++j) {
+    const int64_t pa = oa + 32LL * j;
+    a += __ldcs(S.val + pa) * vec[__ldcs(S.col + pa)];
+  }
+#pragma unroll 4
+  for (int j = k; j < wb; ++j) {
+    const int64_t pb = ob + 32LL * j;
+    b += __ldcs(S.val + pb) * vec[__ldcs(S.col + pb)];
+  }
+  acc_a = a;
+  acc_b = b;
+}
+
 // Group-of-G sum inside a warp (G power of two, runtime).
 __device__ __forceinline__ double gsum(double v, int G) {
   for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
