@@ -72,8 +72,81 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
   }
 }
 
+// SOC derivative applier on register-resident block entries: lane lg of a
+// group of G lanes holds entries i = lg + e G (e < kSocE) (cones.py:740-764).
+constexpr int kSocE = 4;
+
+__device__ __forceinline__ void soc_apply_regs(const double (&z)[kSocE], const double (&in)[kSocE], int dim,
+                                               double nu, int code, int lg, int G, int src, double (&out)[kSocE]) {
+  const double t = __shfl_sync(0xffffffffu, z[0], src);
+  const double dt = __shfl_sync(0xffffffffu, in[0], src);
+  double part = 0.0;
+#pragma unroll
+  for (int e = 0; e < kSocE; ++e) {
+    const int i = lg + e * G;
+    if (i >= 1 && i < dim) part += z[e] * in[e];
+  }
+  for (int o = G >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  const double udu = part, two_nu = 2.0 * nu, tn = t + nu;
+  const double c = (code == 3) ? (t / (nu * nu)) * udu : 0.0;
+#pragma unroll
+  for (int e = 0; e < kSocE; ++e) {
+    const int i = lg + e * G;
+    double v;
+    if (code == 0) v = 0.0;
+    else if (code == 1) v = in[e];
+    else if (code == 2) v = 0.5 * in[e];
+    else v = (i == 0 ? nu * dt + udu : (z[e] * dt + tn * in[e]) - c * z[e]) / two_nu;
+    out[e] = v;
+  }
+}
+
+// Fused F'-step epilogue for a unit of SOC blocks: per block, D Pi t, the
+// row update, and D Pi of the result, all in registers (no CTA barrier).
+template <class Fin>
+__device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, const double *t, Fin fin_row,
+                                             double *dpout) {
+  const int G = u.group, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lg = lane & (G - 1), gw = lane / G, gpw = 32 / G, src = gw * G;
+  for (int base = u.blk0 + warp * gpw; base < u.blk1; base += kWarps * gpw) {
+    const int k = base + gw;
+    const bool valid = k < u.blk1;
+    int dim = 0, code = 0, row = 0;
+    double nu = 1.0;
+    if (valid) {
+      const BlockInfo b = dv.blk[k];
+      dim = b.dim;
+      row = b.row;
+      nu = dv.soc_nu[b.param];
+      code = dv.soc_code[b.param];
+    }
+    double z[kSocE], tv[kSocE], r[kSocE], o[kSocE], d[kSocE];
+#pragma unroll
+    for (int e = 0; e < kSocE; ++e) {
+      const int i = lg + e * G;
+      const bool in = valid && i < dim;
+      z[e] = in ? dv.zmid[row + i] : 0.0;
+      tv[e] = in ? t[row + i] : 0.0;
+    }
+    soc_apply_regs(z, tv, dim, nu, code, lg, G, src, r);
+#pragma unroll
+    for (int e = 0; e < kSocE; ++e) {
+      const int i = lg + e * G;
+      o[e] = (valid && i < dim) ? fin_row(row + i, r[e]) : 0.0;
+    }
+    if (dpout) {
+      soc_apply_regs(z, o, dim, nu, code, lg, G, src, d);
+#pragma unroll
+      for (int e = 0; e < kSocE; ++e) {
+        const int i = lg + e * G;
+        if (valid && i < dim) dpout[row + i] = d[e];
+      }
+    }
+  }
+}
+
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) k_step(Mats M, StepArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
   const bool isx = (int)blockIdx.x < M.nxu;
@@ -126,19 +199,50 @@ __global__ void __launch_bounds__(kThreads) k_step(Mats M, StepArgs a) {
       for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
                [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
       __syncthreads();
-      // r = D Pi t  (blockwise, in the unit)
-      dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
-      // pass 2: (r + w2)/z_N, axpy, norms
-      for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+      // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step
+      auto fin_row = [&](int r, double dpt) {
         const double w = inY[r];
-        const double res = (a.tY2[r] + w) / E.zN;
-        const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+        const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
         outY[r] = o;
         acc[0] += M.b[r] * w;
         acc[2] += o * o;
+        return o;
+      };
+      if (u.cls == CLS_ELEM) {
+        // fused register epilogue: weight read once, both D Pi applications
+        const int kind = M.dpi.blk[u.blk0].kind;
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+          const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
+          const double o = fin_row(r, wgt * a.tY[r]);
+          if (a.dpout) a.dpout[r] = wgt * o;
+        }
+      } else if (u.cls == CLS_TRI) {
+        for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+          const BlockInfo b = M.dpi.blk[k];
+          double D[9];
+#pragma unroll
+          for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
+          const int flip = M.dpi.tri_flip[b.param];
+          const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
+          double r3[3], o3[3], d3[3];
+          tri_apply(D, flip, t3, r3);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
+          if (a.dpout) {
+            tri_apply(D, flip, o3, d3);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
+          }
+        }
+      } else if (u.cls == CLS_SOC && u.group > 0) {
+        soc_epilogue(M.dpi, u, a.tY, fin_row, a.dpout);
+      } else {
+        // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
+        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
+        __syncthreads();
+        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
       }
-      __syncthreads();
-      if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
     }
   }
   double tot[kSlots];
