@@ -52,8 +52,8 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive);
-  if (h_nactive) cudaFreeHost(h_nactive);
+  dev_free(st); dev_free(d_nactive); dev_free(part_t);
+  h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
 // Captured (not instantiated) LSMR graphs per handle, keyed by (jvp, iters).
@@ -80,6 +80,7 @@ Handle::~Handle() {
   sP.release(); sAT.release(); sA.release();
   dev_free(x_rowof); dev_free(y_rowof);
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
+  dev_free(d_tasks); dev_free(d_xt_ptr); dev_free(d_yt_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   ws.release();
   std::lock_guard<std::mutex> g(g_graph_mu);
@@ -198,6 +199,7 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   H.cones.build(per, H.yoff, target_rows_y, st);
   trace("cone table");
   build_sell(H, rpP, rpAT, rpA, st);
+  build_tasks(H, st);
   trace("sell layout");
   H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
   H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
@@ -225,9 +227,10 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.dpu = dev_alloc<double>(H.NY); W.dpv = dev_alloc<double>(H.NY);
   W.tY = dev_alloc<double>(H.NY); W.tY2 = dev_alloc<double>(H.NY);
   W.part = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
+  W.part_t = dev_alloc<double>((size_t)(H.ntx + H.nty + 1) * kSlots);
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
-  QG_CUDA(cudaMallocHost(&W.h_nactive, sizeof(int)));
+  W.h_nactive = nullptr;
   trace("workspace");
 
   // embedding: z = (x, y - s, 1); Pi z; D Pi prep; P xbar, xbar'P xbar
@@ -323,8 +326,17 @@ static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStre
   QG_CUDA(cudaGraphLaunch(se.exec, st));
 }
 
+// One pinned word per host thread for the active-problem count (pinned
+// allocation is expensive; never per handle).
+static int *pinned_word() {
+  static thread_local int *p = nullptr;
+  if (!p) QG_CUDA(cudaMallocHost(&p, sizeof(int)));
+  return p;
+}
+
 static int kernels_per_iter(const Handle &H) {
-  return 6 - (H.nxu() + H.nyu() == 0 ? 3 : 0);
+  // k_spmv<F>, k_spmv<F'> + k_ft_epi, k_update, 3 x k_fin
+  return 7 - (H.nxu() + H.nyu() == 0 ? 4 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
@@ -332,9 +344,10 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
   long long done = 0;
   while (true) {
     launch_count_active(H, st);
-    QG_CUDA(cudaMemcpyAsync(W.h_nactive, W.d_nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int *pinned = pinned_word();
+    QG_CUDA(cudaMemcpyAsync(pinned, W.d_nactive, sizeof(int), cudaMemcpyDeviceToHost, st));
     QG_CUDA(cudaStreamSynchronize(st));
-    if (*W.h_nactive == 0 || done >= cap) break;
+    if (*pinned == 0 || done >= cap) break;
     const long long rem = cap - done;
     // 16 first (early convergence wastes little), then chunks of 64
     const long long want = done == 0 ? std::min<long long>(rem, 16) : rem;

@@ -3,14 +3,18 @@
 // and its transpose, for a whole batch of problems at once.
 //
 // Per iteration:
-//   k_step<F>   u <- s_in * F v  - c_out * u   fused CSR SpMV (P, A', A) + epilogue
+//   k_spmv<F>   u <- s_in F v - c_out u : warp tasks over SELL slices of P, A'
+//               (X rows) and A (Y rows), fused row epilogue, task partials
 //   k_fin       per problem: T component, ||u||, scalars          (lsmr.py:115-118)
-//   k_step<FT>  v <- s_in * F' u - c_out * v   SpMV + D Pi epilogue (x2) per cone block
+//   k_spmv<FT>  X rows of v <- s_in F' u - c_out v ; Y rows: t = A u1 - u_N b - u2
+//   k_ft_epi    per cone block: D Pi t, the row update, D Pi of the result
 //   k_fin       ||v||, Givens recurrences, update coefficients   (lsmr.py:119-171)
 //   k_update    hbar, x, h axpys + ||x||^2 partials               (lsmr.py:142-144, 168)
 //   k_fin       stopping rules                                     (lsmr.py:173-182)
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
+// The SpMV kernels are barrier-free: one warp per task, partial sums per
+// task, reduced per problem in fixed order by k_fin (deterministic).
 #include "dpi_dev.cuh"
 #include "ops_dev.cuh"
 #include "operator.h"
@@ -31,47 +35,100 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
   return L.active && !(is_v_step && L.skip_v);
 }
 
-// ------------------------------------------------------------- op steps --
-// Iterate the rows of a unit: MODE_SELL -> one thread per row over the unit's
-// SELL slices; MODE_LONG -> a group of G lanes per CSR row.  `row(r, s1, s2)`
-// receives the row sums of the one or two matrices (second may be unused).
+// ---------------------------------------------------------- SpMV steps --
+// Rows of one warp task.  TASK_SELL: a pair of slices, one thread per row;
+// TASK_LONG: warp per CSR row.  row(r, s1, s2) gets the row sums of the one
+// or two matrices (s2 = 0 when there is a single matrix).
 template <class RowFn>
-__device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
-                                         const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
-                                         const double *v1, const int32_t *rp2, const int32_t *c2,
-                                         const double *v2, const double *x1, const double *x2, RowFn row) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (u.mode == MODE_SELL) {
-    // warps claim pairs of slices dynamically (balances uneven units)
-    __shared__ int next_slice;
-    if (threadIdx.x == 0) next_slice = u.s0;
-    __syncthreads();
-    while (true) {
-      int s = 0;
-      if (lane == 0) s = atomicAdd(&next_slice, 2);
-      s = __shfl_sync(0xffffffffu, s, 0);
-      if (s >= u.s1) break;
-      const int sb = s + 1 < u.s1 ? s + 1 : -1;
-      const int ra = rowof[(int64_t)s * 32 + lane];
-      const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
-      double a1, b1, a2 = 0.0, b2 = 0.0;
-      sell_dot2(S1, s, sb, lane, x1, a1, b1);
-      if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
-      if (ra >= 0) row(ra, a1, a2);
-      if (rb >= 0) row(rb, b1, b2);
-    }
+__device__ __forceinline__ void task_rows(const Task &T, int lane, const SellView &S1, const SellView *S2,
+                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
+                                          const double *v1, const int32_t *rp2, const int32_t *c2,
+                                          const double *v2, const double *x1, const double *x2, RowFn row) {
+  if (T.kind == TASK_SELL) {
+    const int s = T.a, sb = T.b;
+    const int ra = rowof[(int64_t)s * 32 + lane];
+    const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
+    double a1, b1, a2 = 0.0, b2 = 0.0;
+    sell_dot2(S1, s, sb, lane, x1, a1, b1);
+    if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
+    if (ra >= 0) row(ra, a1, a2);
+    if (rb >= 0) row(rb, b1, b2);
   } else {
-    const int G = 32;
-    for (int r = u.row0 + warp; r < u.row1; r += kWarps) {
-      double s1 = row_dot(rp1, c1, v1, x1, r, lane, G);
-      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, G) : 0.0;
-      s1 = gsum(s1, G);
-      s2 = gsum(s2, G);
+    for (int r = T.a; r < T.b; ++r) {
+      double s1 = row_dot(rp1, c1, v1, x1, r, lane, 32);
+      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, 32) : 0.0;
+      s1 = gsum(s1, 32);
+      s2 = gsum(s2, 32);
       if (lane == 0) row(r, s1, s2);
     }
   }
 }
 
+__device__ __forceinline__ void warp_write_slots(double (&acc)[kSlots], double *slot, int lane) {
+#pragma unroll
+  for (int k = 0; k < kSlots; ++k) acc[k] = warp_sum(acc[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) slot[k] = acc[k];
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) k_spmv(Mats M, StepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (t >= M.ntx + M.nty) return;
+  const Task T = M.tasks[t];
+  double s_in, c_out;
+  if (!lsmr_runs(a, T.prob, s_in, c_out)) return;  // warp-uniform
+  const Embed E = M.emb[T.prob];
+  const double *inX = a.in, *inY = a.in + M.NX;
+  const double wN = a.in[M.NX + M.NY + T.prob];
+  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
+
+  if (t < M.ntx) {
+    const double *x2 = KIND == STEP_F ? a.dpin : inY;
+    task_rows(T, lane, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
+              [&](int r, double s1, double s2) {
+                const double w = inX[r];
+                double res;
+                if (KIND == STEP_F) {
+                  // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
+                  const double o1 = (s1 + s2) + wN * M.q[r];
+                  res = ((o1 - w) + w) / E.zN;
+                  acc[0] += M.Pxbar[r] * w;
+                } else {
+                  // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
+                  const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
+                  res = ((g - w) + w) / E.zN;
+                }
+                acc[1] += M.q[r] * w;
+                const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
+                a.out[r] = o;
+                acc[2] += o * o;
+              });
+  } else if (KIND == STEP_F) {
+    double *outY = a.out + M.NX;
+    const double *oldY = a.old ? a.old + M.NX : nullptr;
+    task_rows(T, lane, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX,
+              nullptr, [&](int r, double s, double) {
+                // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
+                const double o2 = (-s) + wN * M.b[r];
+                const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+                const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+                outY[r] = o;
+                acc[0] += M.b[r] * a.dpin[r];
+                acc[2] += o * o;
+              });
+  } else {
+    // F' Y rows: t = (A w1 - w_N b) - w2, finished per cone block by k_ft_epi
+    task_rows(T, lane, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX,
+              nullptr, [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
+    return;  // no partials: k_ft_epi owns the Y-side sums
+  }
+  warp_write_slots(acc, M.part_t + t * kSlots, lane);
+}
+
+// ------------------------------------------------------ F' epilogue --
 // SOC derivative applier on register-resident block entries: lane lg of a
 // group of G lanes holds entries i = lg + e G (e < kSocE) (cones.py:740-764).
 constexpr int kSocE = 4;
@@ -101,14 +158,14 @@ __device__ __forceinline__ void soc_apply_regs(const double (&z)[kSocE], const d
   }
 }
 
-// Fused F'-step epilogue for a unit of SOC blocks: per block, D Pi t, the
-// row update, and D Pi of the result, all in registers (no CTA barrier).
+// Unit of SOC blocks: per block, D Pi t, the row update, and D Pi of the
+// result, all in registers (no CTA barrier).
 template <class Fin>
 __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, const double *t, Fin fin_row,
                                              double *dpout) {
-  const int G = u.group, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = u.group, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int lg = lane & (G - 1), gw = lane / G, gpw = 32 / G, src = gw * G;
-  for (int base = u.blk0 + warp * gpw; base < u.blk1; base += kWarps * gpw) {
+  for (int base = u.blk0 + warp * gpw; base < u.blk1; base += nw * gpw) {
     const int k = base + gw;
     const bool valid = k < u.blk1;
     int dim = 0, code = 0, row = 0;
@@ -145,111 +202,65 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
   }
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(kThreads, 4) k_step(Mats M, StepArgs a) {
+// One CTA per Y unit: v2 = s_in (D Pi t + w2)/z_N - c_out v2_old ; D Pi v2.
+__global__ void __launch_bounds__(kThreads) k_ft_epi(Mats M, StepArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
-  const bool isx = (int)blockIdx.x < M.nxu;
-  const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
-  const int p = u.prob;
+  const Unit u = M.yu[blockIdx.x];
   double s_in, c_out;
-  if (!lsmr_runs(a, p, s_in, c_out)) return;  // CTA-uniform
-  const Embed E = M.emb[p];
-  const double *inX = a.in, *inY = a.in + M.NX;
-  const double wN = a.in[M.NX + M.NY + p];
+  if (!lsmr_runs(a, u.prob, s_in, c_out)) return;  // CTA-uniform
+  const Embed E = M.emb[u.prob];
+  const double *inY = a.in + M.NX;
+  double *outY = a.out + M.NX;
+  const double *oldY = a.old ? a.old + M.NX : nullptr;
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
-
-  if (isx) {
-    const double *x2 = KIND == STEP_F ? a.dpin : inY;
-    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
-             [&](int r, double s1, double s2) {
-               const double w = inX[r];
-               double res;
-               if (KIND == STEP_F) {
-                 // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
-                 const double o1 = (s1 + s2) + wN * M.q[r];
-                 res = ((o1 - w) + w) / E.zN;
-                 acc[0] += M.Pxbar[r] * w;
-               } else {
-                 // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
-                 const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
-                 res = ((g - w) + w) / E.zN;
-               }
-               acc[1] += M.q[r] * w;
-               const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
-               a.out[r] = o;
-               acc[2] += o * o;
-             });
-  } else {
-    double *outY = a.out + M.NX;
-    const double *oldY = a.old ? a.old + M.NX : nullptr;
-    if (KIND == STEP_F) {
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
-               [&](int r, double s, double) {
-                 // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
-                 const double o2 = (-s) + wN * M.b[r];
-                 const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
-                 const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
-                 outY[r] = o;
-                 acc[0] += M.b[r] * a.dpin[r];
-                 acc[2] += o * o;
-               });
-    } else {
-      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
-               [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
-      __syncthreads();
-      // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step
-      auto fin_row = [&](int r, double dpt) {
-        const double w = inY[r];
-        const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
-        outY[r] = o;
-        acc[0] += M.b[r] * w;
-        acc[2] += o * o;
-        return o;
-      };
-      if (u.cls == CLS_ELEM) {
-        // fused register epilogue: weight read once, both D Pi applications
-        const int kind = M.dpi.blk[u.blk0].kind;
-        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
-          const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
-          const double o = fin_row(r, wgt * a.tY[r]);
-          if (a.dpout) a.dpout[r] = wgt * o;
-        }
-      } else if (u.cls == CLS_TRI) {
-        for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
-          const BlockInfo b = M.dpi.blk[k];
-          double D[9];
+  auto fin_row = [&](int r, double dpt) {
+    const double w = inY[r];
+    const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+    outY[r] = o;
+    acc[0] += M.b[r] * w;
+    acc[2] += o * o;
+    return o;
+  };
+  if (u.cls == CLS_ELEM) {
+    const int kind = M.dpi.blk[u.blk0].kind;
+    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+      const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
+      const double o = fin_row(r, wgt * a.tY[r]);
+      if (a.dpout) a.dpout[r] = wgt * o;
+    }
+  } else if (u.cls == CLS_TRI) {
+    for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+      const BlockInfo b = M.dpi.blk[k];
+      double D[9];
 #pragma unroll
-          for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
-          const int flip = M.dpi.tri_flip[b.param];
-          const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
-          double r3[3], o3[3], d3[3];
-          tri_apply(D, flip, t3, r3);
+      for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
+      const int flip = M.dpi.tri_flip[b.param];
+      const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
+      double r3[3], o3[3], d3[3];
+      tri_apply(D, flip, t3, r3);
 #pragma unroll
-          for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
-          if (a.dpout) {
-            tri_apply(D, flip, o3, d3);
+      for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
+      if (a.dpout) {
+        tri_apply(D, flip, o3, d3);
 #pragma unroll
-            for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
-          }
-        }
-      } else if (u.cls == CLS_SOC && u.group > 0) {
-        soc_epilogue(M.dpi, u, a.tY, fin_row, a.dpout);
-      } else {
-        // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
-        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
-        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
-        __syncthreads();
-        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
+        for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
       }
     }
+  } else if (u.cls == CLS_SOC && u.group > 0) {
+    soc_epilogue(M.dpi, u, a.tY, fin_row, a.dpout);
+  } else {
+    // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
+    dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
+    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
+    __syncthreads();
+    if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
   }
   double tot[kSlots];
   cta_sum_slots(acc, red, tot);
-  if (threadIdx.x == 0 && a.part)
+  if (threadIdx.x == 0)
 #pragma unroll
-    for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
+    for (int k = 0; k < kSlots; ++k) M.part_u[((size_t)M.nxu + blockIdx.x) * kSlots + k] = tot[k];
 }
 
 // -------------------------------------------------------------- update --
@@ -314,17 +325,14 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (p >= a.B) return;
   Lsmr *L = a.st ? a.st + p : nullptr;
   if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
-  if (L && a.phase == PH_STEP_V && L->skip_v) {
-    // fall through: v-step did not run, only the recurrences do
-  }
-  // deterministic per-problem sums of the unit partials
+  // deterministic per-problem sums of the producers' partials (fixed order)
   double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
-  for (int64_t k = M.xu_ptr[p] + lane; k < M.xu_ptr[p + 1]; k += 32)
+  for (int64_t k = a.px_ptr[p] + lane; k < a.px_ptr[p + 1]; k += 32)
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sx[j] += a.part[k * kSlots + j];
-  for (int64_t k = M.yu_ptr[p] + lane; k < M.yu_ptr[p + 1]; k += 32)
+    for (int j = 0; j < kSlots; ++j) sx[j] += a.px[k * kSlots + j];
+  for (int64_t k = a.py_ptr[p] + lane; k < a.py_ptr[p + 1]; k += 32)
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sy[j] += a.part[(M.nxu + k) * kSlots + j];
+    for (int j = 0; j < kSlots; ++j) sy[j] += a.py[k * kSlots + j];
 #pragma unroll
   for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
   if (lane != 0) return;
@@ -549,26 +557,44 @@ Mats make_mats(const Handle &H) {
   M.dpi = H.cones.view();
   M.sP = H.sP.view(); M.sAT = H.sAT.view(); M.sA = H.sA.view();
   M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
+  M.tasks = H.d_tasks; M.ntx = H.ntx; M.nty = H.nty;
+  M.xt_ptr = H.d_xt_ptr; M.yt_ptr = H.d_yt_ptr;
+  M.part_t = H.ws.part_t;
+  M.part_u = H.ws.part;
   return M;
 }
 
 static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
 
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
-  const unsigned grid = (unsigned)(H.nxu() + H.nyu());
-  if (grid == 0) return;
-  const size_t smem = step_smem(H);
-  if (kind == STEP_F) {
-    k_step<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
-  } else {
-    if (smem > 48 * 1024)
-      QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_step<STEP_FT><<<grid, kThreads, smem, st>>>(M, a);
+  const int64_t ntask = H.ntx + H.nty;
+  if (ntask > 0) {
+    const unsigned grid = (unsigned)((ntask + kWarps - 1) / kWarps);
+    if (kind == STEP_F) k_spmv<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
+    else k_spmv<STEP_FT><<<grid, kThreads, 0, st>>>(M, a);
+    QG_LAUNCHED();
   }
-  QG_LAUNCHED();
+  if (kind == STEP_FT && H.nyu() > 0) {
+    const size_t smem = step_smem(H);
+    if (smem > 48 * 1024)
+      QG_CUDA(cudaFuncSetAttribute(k_ft_epi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_ft_epi<<<(unsigned)H.nyu(), kThreads, smem, st>>>(M, a);
+    QG_LAUNCHED();
+  }
 }
 
-void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st) {
+void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
+  FinArgs a = a0;
+  const double *pu = H.ws.part, *pt = H.ws.part_t;
+  if (a.phase == PH_RHS || a.phase == PH_STEP_X) {
+    // unit-based producers (assembly kernels, k_update)
+    a.px = pu; a.px_ptr = H.d_xunit_ptr;
+    a.py = pu + (size_t)H.nxu() * kSlots; a.py_ptr = H.d_yunit_ptr;
+  } else {
+    a.px = pt; a.px_ptr = H.d_xt_ptr;
+    if (a.kind == STEP_F) { a.py = pt; a.py_ptr = H.d_yt_ptr; }
+    else { a.py = pu + (size_t)H.nxu() * kSlots; a.py_ptr = H.d_yunit_ptr; }
+  }
   const unsigned grid = (unsigned)((H.B * 32 + 255) / 256);
   k_fin<<<grid, 256, 0, st>>>(M, a);
   QG_LAUNCHED();

@@ -33,6 +33,10 @@ struct FinArgs {
   const double *old;   // EVec
   double *out;         // EVec (T component written)
   double *h, *hb, *x, *v;
+  // filled by launch_fin: partial-sum arrays and per-problem ranges of the
+  // X-side and Y-side producers of this phase
+  const double *px = nullptr, *py = nullptr;
+  const int64_t *px_ptr = nullptr, *py_ptr = nullptr;
 };
 
 struct UpdArgs {

@@ -92,6 +92,14 @@ struct Unit {
 
 enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1 };
 
+// A warp task of the SpMV steps: a pair of SELL slices (a, b; b = -1 if
+// none) or a range of long CSR rows [a, b) processed warp-per-row.  Tasks
+// never cross problems; one warp per task, no CTA-level synchronisation.
+enum TaskKind : int32_t { TASK_SELL = 0, TASK_LONG = 1 };
+struct Task {
+  int32_t prob, kind, a, b;
+};
+
 // SELL-C-sigma storage (C = 32 = warp width, sigma = the work unit): the rows
 // of a unit are sorted by length (descending) and cut into slices of 32; in
 // slice s entry k of lane l sits at off[s] + 32 k + l, so a warp reads 32

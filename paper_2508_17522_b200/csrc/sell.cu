@@ -195,6 +195,39 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
 
 }  // namespace
 
+void build_tasks(Handle &H, cudaStream_t st) {
+  constexpr int kLongRowsPerTask = 4;
+  H.tasks.clear();
+  auto side = [&](const std::vector<Unit> &units, std::vector<int64_t> &ptr) {
+    ptr.assign(H.B + 1, 0);
+    size_t ui = 0;
+    for (int p = 0; p < H.B; ++p) {
+      ptr[p] = (int64_t)H.tasks.size();
+      for (; ui < units.size() && units[ui].prob == p; ++ui) {
+        const Unit &u = units[ui];
+        if (u.mode == MODE_SELL) {
+          for (int s = u.s0; s < u.s1; s += 2) H.tasks.push_back(Task{p, TASK_SELL, s, s + 1 < u.s1 ? s + 1 : -1});
+        } else {
+          for (int r = u.row0; r < u.row1; r += kLongRowsPerTask)
+            H.tasks.push_back(Task{p, TASK_LONG, r, std::min(u.row1, r + kLongRowsPerTask)});
+        }
+      }
+    }
+    ptr[H.B] = (int64_t)H.tasks.size();
+  };
+  side(H.xunits, H.xt_ptr);
+  H.ntx = (int64_t)H.tasks.size();
+  side(H.cones.units, H.yt_ptr);
+  H.nty = (int64_t)H.tasks.size() - H.ntx;
+  H.d_tasks = dev_alloc<Task>(H.tasks.size());
+  H.d_xt_ptr = dev_alloc<int64_t>(H.B + 1);
+  H.d_yt_ptr = dev_alloc<int64_t>(H.B + 1);
+  if (!H.tasks.empty())
+    QG_CUDA(cudaMemcpyAsync(H.d_tasks, H.tasks.data(), sizeof(Task) * H.tasks.size(), cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(H.d_xt_ptr, H.xt_ptr.data(), sizeof(int64_t) * (H.B + 1), cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(H.d_yt_ptr, H.yt_ptr.data(), sizeof(int64_t) * (H.B + 1), cudaMemcpyHostToDevice, st));
+}
+
 void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
                 const std::vector<int32_t> &rpA, cudaStream_t st) {
   const char *side = std::getenv("QG_SELL_SIDE");  // diagnostics: "x" or "y" only
