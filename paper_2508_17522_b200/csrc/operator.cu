@@ -73,16 +73,9 @@ __device__ __forceinline__ void warp_write_slots(double (&acc)[kSlots], double *
 }
 
 template <int KIND>
-__global__ void __launch_bounds__(kThreads) k_spmv(Mats M, StepArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t t = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (t >= M.ntx + M.nty) return;
-  const Task T = M.tasks[t];
-  double s_in, c_out;
-  if (!lsmr_runs(a, T.prob, s_in, c_out)) return;  // warp-uniform
-  const Embed E = M.emb[T.prob];
-  const double *inX = a.in, *inY = a.in + M.NX;
-  const double wN = a.in[M.NX + M.NY + T.prob];
+__device__ __forceinline__ void spmv_task(const Mats &M, const StepArgs &a, const Task &T, int64_t t, int lane,
+                                          double s_in, double c_out, double wN, const Embed &E, const double *inX,
+                                          const double *inY) {
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
 
   if (t < M.ntx) {
@@ -126,6 +119,33 @@ __global__ void __launch_bounds__(kThreads) k_spmv(Mats M, StepArgs a) {
     return;  // no partials: k_ft_epi owns the Y-side sums
   }
   warp_write_slots(acc, M.part_t + t * kSlots, lane);
+}
+
+// Persistent warps: warp g owns the contiguous task range [g k, (g+1) k), so
+// consecutive tasks mostly share a problem and the per-problem prologue
+// (LSMR coefficients, embedding constants) is loaded once per problem.
+template <int KIND>
+__global__ void __launch_bounds__(kThreads) k_spmv(Mats M, StepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ntask = M.ntx + M.nty;
+  const int64_t nwarp = (int64_t)gridDim.x * kWarps, gwarp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const int64_t per = (ntask + nwarp - 1) / nwarp;
+  const int64_t t0 = gwarp * per, t1 = t0 + per < ntask ? t0 + per : ntask;
+  int cur = -1;
+  bool run = false;
+  double s_in = 1.0, c_out = 0.0, wN = 0.0;
+  Embed E{};
+  const double *inX = a.in, *inY = a.in + M.NX;
+  for (int64_t t = t0; t < t1; ++t) {
+    const Task T = M.tasks[t];
+    if (T.prob != cur) {
+      cur = T.prob;
+      run = lsmr_runs(a, cur, s_in, c_out);
+      E = M.emb[cur];
+      wN = a.in[M.NX + M.NY + cur];
+    }
+    if (run) spmv_task<KIND>(M, a, T, t, lane, s_in, c_out, wN, E, inX, inY);
+  }
 }
 
 // ------------------------------------------------------ F' epilogue --
@@ -569,7 +589,11 @@ static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cone
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
   const int64_t ntask = H.ntx + H.nty;
   if (ntask > 0) {
-    const unsigned grid = (unsigned)((ntask + kWarps - 1) / kWarps);
+    // persistent grid: 4 CTAs per SM (register-limited occupancy), >= 1 task per warp
+    static int nsm = 0;
+    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 4);
+    const unsigned grid = (unsigned)std::min<int64_t>(want, (ntask + kWarps - 1) / kWarps);
     if (kind == STEP_F) k_spmv<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
     else k_spmv<STEP_FT><<<grid, kThreads, 0, st>>>(M, a);
     QG_LAUNCHED();
