@@ -335,8 +335,8 @@ static int *pinned_word() {
 }
 
 static int kernels_per_iter(const Handle &H) {
-  // k_spmv<F>, k_spmv<F'> + k_ft_epi, k_update, 3 x k_fin
-  return 7 - (H.nxu() + H.nyu() == 0 ? 4 : 0);
+  // k_step<F>, k_step<F'>, k_update, 3 x k_fin
+  return 6 - (H.nxu() + H.nyu() == 0 ? 3 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {

@@ -279,13 +279,10 @@ void ConeTable::build(const std::vector<std::vector<qg_cone_block>> &per_prob, c
           ++e;
         }
         Unit un{p, b.row, (int32_t)(b.row + rows), (int32_t)bi, (int32_t)e, cls};
-        if (cls == CLS_SOC) {  // lanes per block for the fused register epilogue (<= 4 entries per lane)
+        if (cls == CLS_SOC) {  // thread-per-block fused epilogue for small SOC blocks
           int maxdim = 0;
           for (int64_t k = bi; k < e; ++k) maxdim = std::max(maxdim, (int)h_blk[k].dim);
-          int g = 1;
-          while (g < 32 && g < maxdim) g <<= 1;
-          un.group = maxdim <= 4 * 32 ? std::max(g, (maxdim + 3) / 4 > 32 ? 32 : g) : 0;
-          if (un.group && (maxdim + un.group - 1) / un.group > 4) un.group = 0;
+          un.group = maxdim <= 32 ? 1 : 0;
         }
         units.push_back(un);
         bi = e;

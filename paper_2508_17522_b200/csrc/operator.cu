@@ -3,18 +3,14 @@
 // and its transpose, for a whole batch of problems at once.
 //
 // Per iteration:
-//   k_spmv<F>   u <- s_in F v - c_out u : warp tasks over SELL slices of P, A'
-//               (X rows) and A (Y rows), fused row epilogue, task partials
+//   k_step<F>   u <- s_in * F v  - c_out * u   fused CSR SpMV (P, A', A) + epilogue
 //   k_fin       per problem: T component, ||u||, scalars          (lsmr.py:115-118)
-//   k_spmv<FT>  X rows of v <- s_in F' u - c_out v ; Y rows: t = A u1 - u_N b - u2
-//   k_ft_epi    per cone block: D Pi t, the row update, D Pi of the result
+//   k_step<FT>  v <- s_in * F' u - c_out * v   SpMV + D Pi epilogue (x2) per cone block
 //   k_fin       ||v||, Givens recurrences, update coefficients   (lsmr.py:119-171)
 //   k_update    hbar, x, h axpys + ||x||^2 partials               (lsmr.py:142-144, 168)
 //   k_fin       stopping rules                                     (lsmr.py:173-182)
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
-// The SpMV kernels are barrier-free: one warp per task, partial sums per
-// task, reduced per problem in fixed order by k_fin (deterministic).
 #include "dpi_dev.cuh"
 #include "ops_dev.cuh"
 #include "operator.h"
@@ -35,252 +31,191 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
   return L.active && !(is_v_step && L.skip_v);
 }
 
-// ---------------------------------------------------------- SpMV steps --
-// Rows of one warp task.  TASK_SELL: a pair of slices, one thread per row;
-// TASK_LONG: warp per CSR row.  row(r, s1, s2) gets the row sums of the one
-// or two matrices (s2 = 0 when there is a single matrix).
+// ------------------------------------------------------------- op steps --
+// Iterate the rows of a unit: MODE_SELL -> one thread per row over the unit's
+// SELL slices; MODE_LONG -> a group of G lanes per CSR row.  `row(r, s1, s2)`
+// receives the row sums of the one or two matrices (second may be unused).
 template <class RowFn>
-__device__ __forceinline__ void task_rows(const Task &T, int lane, const SellView &S1, const SellView *S2,
-                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
-                                          const double *v1, const int32_t *rp2, const int32_t *c2,
-                                          const double *v2, const double *x1, const double *x2, RowFn row) {
-  if (T.kind == TASK_SELL) {
-    const int s = T.a, sb = T.b;
-    const int ra = rowof[(int64_t)s * 32 + lane];
-    const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
-    double a1, b1, a2 = 0.0, b2 = 0.0;
-    sell_dot2(S1, s, sb, lane, x1, a1, b1);
-    if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
-    if (ra >= 0) row(ra, a1, a2);
-    if (rb >= 0) row(rb, b1, b2);
+__device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
+                                         const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
+                                         const double *v1, const int32_t *rp2, const int32_t *c2,
+                                         const double *v2, const double *x1, const double *x2, RowFn row) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (u.mode == MODE_SELL) {
+    // warps claim pairs of slices dynamically (balances uneven units)
+    __shared__ int next_slice;
+    if (threadIdx.x == 0) next_slice = u.s0;
+    __syncthreads();
+    while (true) {
+      int s = 0;
+      if (lane == 0) s = atomicAdd(&next_slice, 2);
+      s = __shfl_sync(0xffffffffu, s, 0);
+      if (s >= u.s1) break;
+      const int sb = s + 1 < u.s1 ? s + 1 : -1;
+      const int ra = rowof[(int64_t)s * 32 + lane];
+      const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
+      double a1, b1, a2 = 0.0, b2 = 0.0;
+      sell_dot2(S1, s, sb, lane, x1, a1, b1);
+      if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
+      if (ra >= 0) row(ra, a1, a2);
+      if (rb >= 0) row(rb, b1, b2);
+    }
   } else {
-    for (int r = T.a; r < T.b; ++r) {
-      double s1 = row_dot(rp1, c1, v1, x1, r, lane, 32);
-      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, 32) : 0.0;
-      s1 = gsum(s1, 32);
-      s2 = gsum(s2, 32);
+    const int G = 32;
+    for (int r = u.row0 + warp; r < u.row1; r += kWarps) {
+      double s1 = row_dot(rp1, c1, v1, x1, r, lane, G);
+      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, G) : 0.0;
+      s1 = gsum(s1, G);
+      s2 = gsum(s2, G);
       if (lane == 0) row(r, s1, s2);
     }
   }
 }
 
-__device__ __forceinline__ void warp_write_slots(double (&acc)[kSlots], double *slot, int lane) {
-#pragma unroll
-  for (int k = 0; k < kSlots; ++k) acc[k] = warp_sum(acc[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < kSlots; ++k) slot[k] = acc[k];
+// F'-step epilogue for a unit of SOC blocks of dim <= 32: one thread per
+// block (cones.py:740-764 applied twice): udu = u'dt ; r = D Pi t ; o = row
+// update ; udu2 = u'o ; D Pi o.  Entries stream through L1 in three short
+// passes with independent loads (no shuffles, no CTA barrier).
+__device__ __forceinline__ double soc_entry(int code, int i, double nu, double t0, double zi, double di,
+                                            double dt, double udu) {
+  if (code == 0) return 0.0;
+  if (code == 1) return di;
+  if (code == 2) return 0.5 * di;
+  const double two_nu = 2.0 * nu;
+  if (i == 0) return (nu * dt + udu) / two_nu;
+  const double c = (t0 / (nu * nu)) * udu;
+  return ((zi * dt + (t0 + nu) * di) - c * zi) / two_nu;
 }
 
-template <int KIND>
-__device__ __forceinline__ void spmv_task(const Mats &M, const StepArgs &a, const Task &T, int64_t t, int lane,
-                                          double s_in, double c_out, double wN, const Embed &E, const double *inX,
-                                          const double *inY) {
-  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
-
-  if (t < M.ntx) {
-    const double *x2 = KIND == STEP_F ? a.dpin : inY;
-    task_rows(T, lane, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
-              [&](int r, double s1, double s2) {
-                const double w = inX[r];
-                double res;
-                if (KIND == STEP_F) {
-                  // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
-                  const double o1 = (s1 + s2) + wN * M.q[r];
-                  res = ((o1 - w) + w) / E.zN;
-                  acc[0] += M.Pxbar[r] * w;
-                } else {
-                  // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
-                  const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
-                  res = ((g - w) + w) / E.zN;
-                }
-                acc[1] += M.q[r] * w;
-                const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
-                a.out[r] = o;
-                acc[2] += o * o;
-              });
-  } else if (KIND == STEP_F) {
-    double *outY = a.out + M.NX;
-    const double *oldY = a.old ? a.old + M.NX : nullptr;
-    task_rows(T, lane, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX,
-              nullptr, [&](int r, double s, double) {
-                // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
-                const double o2 = (-s) + wN * M.b[r];
-                const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
-                const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
-                outY[r] = o;
-                acc[0] += M.b[r] * a.dpin[r];
-                acc[2] += o * o;
-              });
-  } else {
-    // F' Y rows: t = (A w1 - w_N b) - w2, finished per cone block by k_ft_epi
-    task_rows(T, lane, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX,
-              nullptr, [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
-    return;  // no partials: k_ft_epi owns the Y-side sums
-  }
-  warp_write_slots(acc, M.part_t + t * kSlots, lane);
-}
-
-// Persistent warps: warp g owns the contiguous task range [g k, (g+1) k), so
-// consecutive tasks mostly share a problem and the per-problem prologue
-// (LSMR coefficients, embedding constants) is loaded once per problem.
-template <int KIND>
-__global__ void __launch_bounds__(kThreads) k_spmv(Mats M, StepArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t ntask = M.ntx + M.nty;
-  const int64_t nwarp = (int64_t)gridDim.x * kWarps, gwarp = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const int64_t per = (ntask + nwarp - 1) / nwarp;
-  const int64_t t0 = gwarp * per, t1 = t0 + per < ntask ? t0 + per : ntask;
-  int cur = -1;
-  bool run = false;
-  double s_in = 1.0, c_out = 0.0, wN = 0.0;
-  Embed E{};
-  const double *inX = a.in, *inY = a.in + M.NX;
-  for (int64_t t = t0; t < t1; ++t) {
-    const Task T = M.tasks[t];
-    if (T.prob != cur) {
-      cur = T.prob;
-      run = lsmr_runs(a, cur, s_in, c_out);
-      E = M.emb[cur];
-      wN = a.in[M.NX + M.NY + cur];
-    }
-    if (run) spmv_task<KIND>(M, a, T, t, lane, s_in, c_out, wN, E, inX, inY);
-  }
-}
-
-// ------------------------------------------------------ F' epilogue --
-// SOC derivative applier on register-resident block entries: lane lg of a
-// group of G lanes holds entries i = lg + e G (e < kSocE) (cones.py:740-764).
-constexpr int kSocE = 4;
-
-__device__ __forceinline__ void soc_apply_regs(const double (&z)[kSocE], const double (&in)[kSocE], int dim,
-                                               double nu, int code, int lg, int G, int src, double (&out)[kSocE]) {
-  const double t = __shfl_sync(0xffffffffu, z[0], src);
-  const double dt = __shfl_sync(0xffffffffu, in[0], src);
-  double part = 0.0;
-#pragma unroll
-  for (int e = 0; e < kSocE; ++e) {
-    const int i = lg + e * G;
-    if (i >= 1 && i < dim) part += z[e] * in[e];
-  }
-  for (int o = G >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-  const double udu = part, two_nu = 2.0 * nu, tn = t + nu;
-  const double c = (code == 3) ? (t / (nu * nu)) * udu : 0.0;
-#pragma unroll
-  for (int e = 0; e < kSocE; ++e) {
-    const int i = lg + e * G;
-    double v;
-    if (code == 0) v = 0.0;
-    else if (code == 1) v = in[e];
-    else if (code == 2) v = 0.5 * in[e];
-    else v = (i == 0 ? nu * dt + udu : (z[e] * dt + tn * in[e]) - c * z[e]) / two_nu;
-    out[e] = v;
-  }
-}
-
-// Unit of SOC blocks: per block, D Pi t, the row update, and D Pi of the
-// result, all in registers (no CTA barrier).
 template <class Fin>
 __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, const double *t, Fin fin_row,
-                                             double *dpout) {
-  const int G = u.group, lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int lg = lane & (G - 1), gw = lane / G, gpw = 32 / G, src = gw * G;
-  for (int base = u.blk0 + warp * gpw; base < u.blk1; base += nw * gpw) {
-    const int k = base + gw;
-    const bool valid = k < u.blk1;
-    int dim = 0, code = 0, row = 0;
-    double nu = 1.0;
-    if (valid) {
-      const BlockInfo b = dv.blk[k];
-      dim = b.dim;
-      row = b.row;
-      nu = dv.soc_nu[b.param];
-      code = dv.soc_code[b.param];
+                                             const double *outY, double *dpout) {
+  for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+    const BlockInfo b = dv.blk[k];
+    const int dim = b.dim, row = b.row, code = dv.soc_code[b.param];
+    const double nu = dv.soc_nu[b.param];
+    const double *z = dv.zmid + row, *tt = t + row;
+    const double t0 = z[0], dt = tt[0];
+    double udu = 0.0;
+    for (int i = 1; i < dim; ++i) udu += z[i] * tt[i];
+    double o0 = 0.0, udu2 = 0.0;
+    for (int i = 0; i < dim; ++i) {
+      const double o = fin_row(row + i, soc_entry(code, i, nu, t0, z[i], tt[i], dt, udu));
+      if (i == 0) o0 = o; else udu2 += z[i] * o;
     }
-    double z[kSocE], tv[kSocE], r[kSocE], o[kSocE], d[kSocE];
-#pragma unroll
-    for (int e = 0; e < kSocE; ++e) {
-      const int i = lg + e * G;
-      const bool in = valid && i < dim;
-      z[e] = in ? dv.zmid[row + i] : 0.0;
-      tv[e] = in ? t[row + i] : 0.0;
-    }
-    soc_apply_regs(z, tv, dim, nu, code, lg, G, src, r);
-#pragma unroll
-    for (int e = 0; e < kSocE; ++e) {
-      const int i = lg + e * G;
-      o[e] = (valid && i < dim) ? fin_row(row + i, r[e]) : 0.0;
-    }
-    if (dpout) {
-      soc_apply_regs(z, o, dim, nu, code, lg, G, src, d);
-#pragma unroll
-      for (int e = 0; e < kSocE; ++e) {
-        const int i = lg + e * G;
-        if (valid && i < dim) dpout[row + i] = d[e];
+    if (dpout)
+      for (int i = 0; i < dim; ++i) {
+        const double oi = i == 0 ? o0 : outY[row + i];
+        dpout[row + i] = soc_entry(code, i, nu, t0, z[i], oi, o0, udu2);
       }
-    }
   }
 }
 
-// One CTA per Y unit: v2 = s_in (D Pi t + w2)/z_N - c_out v2_old ; D Pi v2.
-__global__ void __launch_bounds__(kThreads) k_ft_epi(Mats M, StepArgs a) {
+template <int KIND>
+__global__ void __launch_bounds__(kThreads, 4) k_step(Mats M, StepArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
-  const Unit u = M.yu[blockIdx.x];
+  const bool isx = (int)blockIdx.x < M.nxu;
+  const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
+  const int p = u.prob;
   double s_in, c_out;
-  if (!lsmr_runs(a, u.prob, s_in, c_out)) return;  // CTA-uniform
-  const Embed E = M.emb[u.prob];
-  const double *inY = a.in + M.NX;
-  double *outY = a.out + M.NX;
-  const double *oldY = a.old ? a.old + M.NX : nullptr;
+  if (!lsmr_runs(a, p, s_in, c_out)) return;  // CTA-uniform
+  const Embed E = M.emb[p];
+  const double *inX = a.in, *inY = a.in + M.NX;
+  const double wN = a.in[M.NX + M.NY + p];
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
-  auto fin_row = [&](int r, double dpt) {
-    const double w = inY[r];
-    const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
-    outY[r] = o;
-    acc[0] += M.b[r] * w;
-    acc[2] += o * o;
-    return o;
-  };
-  if (u.cls == CLS_ELEM) {
-    const int kind = M.dpi.blk[u.blk0].kind;
-    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
-      const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
-      const double o = fin_row(r, wgt * a.tY[r]);
-      if (a.dpout) a.dpout[r] = wgt * o;
-    }
-  } else if (u.cls == CLS_TRI) {
-    for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
-      const BlockInfo b = M.dpi.blk[k];
-      double D[9];
+
+  if (isx) {
+    const double *x2 = KIND == STEP_F ? a.dpin : inY;
+    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
+             [&](int r, double s1, double s2) {
+               const double w = inX[r];
+               double res;
+               if (KIND == STEP_F) {
+                 // out1 = P w1 + A' (D Pi w)_2 + w_N q ; (out - v + w)/z_N with v1 = w1
+                 const double o1 = (s1 + s2) + wN * M.q[r];
+                 res = ((o1 - w) + w) / E.zN;
+                 acc[0] += M.Pxbar[r] * w;
+               } else {
+                 // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
+                 const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
+                 res = ((g - w) + w) / E.zN;
+               }
+               acc[1] += M.q[r] * w;
+               const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
+               a.out[r] = o;
+               acc[2] += o * o;
+             });
+  } else {
+    double *outY = a.out + M.NX;
+    const double *oldY = a.old ? a.old + M.NX : nullptr;
+    if (KIND == STEP_F) {
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+               [&](int r, double s, double) {
+                 // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
+                 const double o2 = (-s) + wN * M.b[r];
+                 const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+                 const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+                 outY[r] = o;
+                 acc[0] += M.b[r] * a.dpin[r];
+                 acc[2] += o * o;
+               });
+    } else {
+      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+               [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
+      __syncthreads();
+      // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step
+      auto fin_row = [&](int r, double dpt) {
+        const double w = inY[r];
+        const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+        outY[r] = o;
+        acc[0] += M.b[r] * w;
+        acc[2] += o * o;
+        return o;
+      };
+      if (u.cls == CLS_ELEM) {
+        // fused register epilogue: weight read once, both D Pi applications
+        const int kind = M.dpi.blk[u.blk0].kind;
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+          const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
+          const double o = fin_row(r, wgt * a.tY[r]);
+          if (a.dpout) a.dpout[r] = wgt * o;
+        }
+      } else if (u.cls == CLS_TRI) {
+        for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+          const BlockInfo b = M.dpi.blk[k];
+          double D[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
-      const int flip = M.dpi.tri_flip[b.param];
-      const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
-      double r3[3], o3[3], d3[3];
-      tri_apply(D, flip, t3, r3);
+          for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
+          const int flip = M.dpi.tri_flip[b.param];
+          const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
+          double r3[3], o3[3], d3[3];
+          tri_apply(D, flip, t3, r3);
 #pragma unroll
-      for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
-      if (a.dpout) {
-        tri_apply(D, flip, o3, d3);
+          for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
+          if (a.dpout) {
+            tri_apply(D, flip, o3, d3);
 #pragma unroll
-        for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
+            for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
+          }
+        }
+      } else if (u.cls == CLS_SOC && u.group > 0) {
+        soc_epilogue(M.dpi, u, a.tY, fin_row, outY, a.dpout);
+      } else {
+        // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
+        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
+        __syncthreads();
+        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
       }
     }
-  } else if (u.cls == CLS_SOC && u.group > 0) {
-    soc_epilogue(M.dpi, u, a.tY, fin_row, a.dpout);
-  } else {
-    // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
-    dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
-    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
-    __syncthreads();
-    if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
   }
   double tot[kSlots];
   cta_sum_slots(acc, red, tot);
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0 && a.part)
 #pragma unroll
-    for (int k = 0; k < kSlots; ++k) M.part_u[((size_t)M.nxu + blockIdx.x) * kSlots + k] = tot[k];
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
 }
 
 // -------------------------------------------------------------- update --
@@ -345,6 +280,9 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (p >= a.B) return;
   Lsmr *L = a.st ? a.st + p : nullptr;
   if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
+  if (L && a.phase == PH_STEP_V && L->skip_v) {
+    // fall through: v-step did not run, only the recurrences do
+  }
   // deterministic per-problem sums of the producers' partials (fixed order)
   double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
   for (int64_t k = a.px_ptr[p] + lane; k < a.px_ptr[p + 1]; k += 32)
@@ -587,38 +525,25 @@ Mats make_mats(const Handle &H) {
 static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
 
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
-  const int64_t ntask = H.ntx + H.nty;
-  if (ntask > 0) {
-    // persistent grid: 4 CTAs per SM (register-limited occupancy), >= 1 task per warp
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t want = std::max<int64_t>(1, (int64_t)nsm * 4);
-    const unsigned grid = (unsigned)std::min<int64_t>(want, (ntask + kWarps - 1) / kWarps);
-    if (kind == STEP_F) k_spmv<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
-    else k_spmv<STEP_FT><<<grid, kThreads, 0, st>>>(M, a);
-    QG_LAUNCHED();
-  }
-  if (kind == STEP_FT && H.nyu() > 0) {
-    const size_t smem = step_smem(H);
+  const unsigned grid = (unsigned)(H.nxu() + H.nyu());
+  if (grid == 0) return;
+  const size_t smem = step_smem(H);
+  if (kind == STEP_F) {
+    k_step<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
+  } else {
     if (smem > 48 * 1024)
-      QG_CUDA(cudaFuncSetAttribute(k_ft_epi, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_ft_epi<<<(unsigned)H.nyu(), kThreads, smem, st>>>(M, a);
-    QG_LAUNCHED();
+      QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_step<STEP_FT><<<grid, kThreads, smem, st>>>(M, a);
   }
+  QG_LAUNCHED();
 }
 
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
-  FinArgs a = a0;
-  const double *pu = H.ws.part, *pt = H.ws.part_t;
-  if (a.phase == PH_RHS || a.phase == PH_STEP_X) {
-    // unit-based producers (assembly kernels, k_update)
-    a.px = pu; a.px_ptr = H.d_xunit_ptr;
-    a.py = pu + (size_t)H.nxu() * kSlots; a.py_ptr = H.d_yunit_ptr;
-  } else {
-    a.px = pt; a.px_ptr = H.d_xt_ptr;
-    if (a.kind == STEP_F) { a.py = pt; a.py_ptr = H.d_yt_ptr; }
-    else { a.py = pu + (size_t)H.nxu() * kSlots; a.py_ptr = H.d_yunit_ptr; }
-  }
+  FinArgs a = a0;  // every producer writes one slot per work unit: X units, then Y units
+  a.px = H.ws.part;
+  a.px_ptr = H.d_xunit_ptr;
+  a.py = H.ws.part + (size_t)H.nxu() * kSlots;
+  a.py_ptr = H.d_yunit_ptr;
   const unsigned grid = (unsigned)((H.B * 32 + 255) / 256);
   k_fin<<<grid, 256, 0, st>>>(M, a);
   QG_LAUNCHED();

@@ -87,7 +87,7 @@ struct Unit {
   int32_t cls;
   int32_t mode;    // MODE_SELL: thread-per-row over SELL slices [s0, s1); MODE_LONG: warp-per-row CSR
   int32_t s0, s1;
-  int32_t group;   // SOC units: lanes per block in the fused epilogue (power of 2 <= 32; 0 = generic path)
+  int32_t group;   // SOC units: 1 = thread-per-block fused epilogue (dims <= 32); 0 = generic CTA path
 };
 
 enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1 };
