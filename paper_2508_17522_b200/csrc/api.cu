@@ -266,8 +266,15 @@ struct LoopVecs {
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
   Workspace &W = H.ws;
   const int ku = jvp ? STEP_F : STEP_FT, kv = jvp ? STEP_FT : STEP_F;
+  // The vector update of iteration k (hbar, x, h) runs fused into the u-step
+  // kernel of iteration k+1 (which streams v_k anyway), and its stopping
+  // test runs at the head of that iteration's PH_STEP_U finalize; the last
+  // iteration's update is flushed by lsmr_flush().  4 launches / iteration.
   for (int i = 0; i < iters; ++i) {
     StepArgs su{W.v, W.dpv, W.u, W.u, ku == STEP_FT ? W.dpu : nullptr, W.tY, W.tY2, W.st, 0, W.part};
+    su.upd_h = W.h;
+    su.upd_hb = W.hb;
+    su.upd_x = W.x;
     launch_step(H, M, ku, su, st);
     FinArgs fu{H.B, PH_STEP_U, ku, W.st, W.part, W.v, W.u, W.u, W.h, W.hb, W.x, W.v};
     launch_fin(H, M, fu, st);
@@ -275,11 +282,18 @@ static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStr
     launch_step(H, M, kv, sv, st);
     FinArgs fv{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
     launch_fin(H, M, fv, st);
-    UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
-    launch_update(H, M, ua, st);
-    FinArgs fx{H.B, PH_STEP_X, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
-    launch_fin(H, M, fx, st);
   }
+}
+
+// Apply the pending update of the last completed iteration and its stopping
+// test (problems that hit the cap are the only ones still active here).
+static void lsmr_flush(Handle &H, const Mats &M, bool jvp, cudaStream_t st) {
+  Workspace &W = H.ws;
+  const int kv = jvp ? STEP_FT : STEP_F;
+  UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
+  launch_update(H, M, ua, st);
+  FinArgs fx{H.B, PH_STEP_X, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
+  launch_fin(H, M, fx, st);
 }
 
 static cudaGraph_t capture_graph(Handle &H, const Mats &M, bool jvp, int iters) {
@@ -335,8 +349,8 @@ static int *pinned_word() {
 }
 
 static int kernels_per_iter(const Handle &H) {
-  // k_step<F>, k_step<F'>, k_update, 3 x k_fin
-  return 6 - (H.nxu() + H.nyu() == 0 ? 3 : 0);
+  // k_step<F>, k_step<F'> (one carries the deferred update), 2 x k_fin
+  return 4 - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
@@ -413,6 +427,7 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
   UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
   launch_update(H, M, ua, st);
   run_lsmr_loop(H, M, jvp, cap, st);
+  lsmr_flush(H, M, jvp, st);
 }
 
 }  // namespace qg

@@ -125,6 +125,22 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(Mats M, StepArgs a) {
   const double wN = a.in[M.NX + M.NY + p];
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
 
+  // deferred vector update of the previous iteration over the unit's own rows
+  // (in = v_k on the u-step): lsmr.py:142-144, ||x||^2 partial in slot 3
+  const Lsmr *L = a.st ? a.st + p : nullptr;
+  if (a.upd_h && L && L->itn > 0) {
+    const double c1 = L->c_hbar, c2 = L->c_x, c3 = L->c_h, sv = L->s_v;
+    const int64_t off = isx ? 0 : M.NX;
+    for (int64_t r = off + u.row0 + threadIdx.x; r < off + u.row1; r += blockDim.x) {
+      const double hb = a.upd_h[r] - c1 * a.upd_hb[r];
+      const double x = a.upd_x[r] + c2 * hb;
+      a.upd_h[r] = a.in[r] * sv - c3 * a.upd_h[r];
+      a.upd_hb[r] = hb;
+      a.upd_x[r] = x;
+      acc[3] += x * x;
+    }
+  }
+
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
@@ -274,6 +290,32 @@ __device__ __forceinline__ double t_component(int kind, const Embed &E, double w
   return (E.last * (gN - wN) + wN) / E.zN;
 }
 
+// Stopping rules after iteration itn with ||x||^2 = xx + xN^2 (lsmr.py:168-184).
+// Returns true when the solve ended (problem deactivated).
+__device__ __forceinline__ bool stop_test(Lsmr *L, double xx, double xN) {
+  const double normx = sqrt(xx + xN * xN);
+  L->normx = normx;
+  const double normr = L->normr, normar = L->normar, normA = L->normA, normb = L->normb;
+  if (!(isfinite(normr) && isfinite(normar) && isfinite(normx))) {
+    L->status = QG_ERR_NUMERICAL;
+    L->active = 0;
+    return true;
+  }
+  bool stop = false;
+  if (normar == 0.0) stop = true;
+  else {
+    const double test1 = normr / normb;
+    const double test2 = normr > 0.0 ? normar / (normA * normr) : 0.0;
+    const double rtol = L->btol + L->atol * normA * normx / normb;
+    const double t1 = test1 / (1.0 + normA * normx / normb);
+    if (1.0 + test2 <= 1.0 || 1.0 + t1 <= 1.0) stop = true;
+    else if (test2 <= L->atol || test1 <= rtol) stop = true;
+  }
+  if (stop) { L->active = 0; L->converged = 1; return true; }
+  if (L->itn >= L->max_iter) { L->active = 0; L->converged = 0; return true; }
+  return false;
+}
+
 __global__ void k_fin(Mats M, FinArgs a) {
   const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
@@ -369,6 +411,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
     return;
   }
   if (a.phase == PH_STEP_U) {
+    if (L->itn > 0 && stop_test(L, sx[3] + sy[3], a.x[T])) return;  // iteration itn ended the solve
     L->itn += 1;
     const double uN = L->s_in * t_component(a.kind, E, a.in[T], sx, sy) - L->c_out * a.old[T];
     a.out[T] = uN;
@@ -452,29 +495,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
     L->c_out = alpha * L->s_u;
     return;
   }
-  if (a.phase == PH_STEP_X) {   // lsmr.py:168-184
-    const double xN = a.x[T];
-    const double normx = sqrt((sx[0] + sy[0]) + xN * xN);
-    L->normx = normx;
-    const double normr = L->normr, normar = L->normar, normA = L->normA, normb = L->normb;
-    if (!(isfinite(normr) && isfinite(normar) && isfinite(normx))) {
-      L->status = QG_ERR_NUMERICAL;
-      L->active = 0;
-      return;
-    }
-    bool stop = false;
-    if (normar == 0.0) stop = true;
-    else {
-      const double test1 = normr / normb;
-      const double test2 = normr > 0.0 ? normar / (normA * normr) : 0.0;
-      const double rtol = L->btol + L->atol * normA * normx / normb;
-      const double t1 = test1 / (1.0 + normA * normx / normb);
-      if (1.0 + test2 <= 1.0 || 1.0 + t1 <= 1.0) stop = true;
-      else if (test2 <= L->atol || test1 <= rtol) stop = true;
-    }
-    if (stop) { L->active = 0; L->converged = 1; }
-    else if (L->itn >= L->max_iter) { L->active = 0; L->converged = 0; }
-  }
+  if (a.phase == PH_STEP_X) stop_test(L, sx[0] + sy[0], a.x[T]);
 }
 
 __global__ void k_count_active(const Lsmr *st, int B, int *out) {

@@ -21,6 +21,10 @@ struct StepArgs {
   int is_v_step;
   double *part;
   double fixed_s_in = 0.0, fixed_c_out = 0.0;  // used when st == null (0 -> 1, 0)
+  // deferred LSMR vector update of the previous iteration (u-step only):
+  // hbar = h - c1 hbar ; x += c2 hbar ; h = in s_v - c3 h over the unit's own
+  // rows, ||x||^2 partial in slot 3 (lsmr.py:142-144, 168)
+  double *upd_h = nullptr, *upd_hb = nullptr, *upd_x = nullptr;
 };
 
 struct FinArgs {
