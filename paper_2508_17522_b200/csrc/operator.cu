@@ -62,7 +62,7 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     }
   } else {
     const int G = 32;
-    for (int r = u.row0 + warp; r < u.row1; r += kWarps) {
+    for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
       double s1 = row_dot(rp1, c1, v1, x1, r, lane, G);
       double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, G) : 0.0;
       s1 = gsum(s1, G);
@@ -111,8 +111,12 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
   }
 }
 
+// 128-thread CTAs: more slice pairs per warp inside a unit (smaller tail at the
+// closing reduction) at the same register-limited occupancy (8 CTAs/SM).
+constexpr int kStepThreads = 128;
+
 template <int KIND>
-__global__ void __launch_bounds__(kThreads, 4) k_step(Mats M, StepArgs a) {
+__global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
   const bool isx = (int)blockIdx.x < M.nxu;
@@ -550,11 +554,11 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
   if (grid == 0) return;
   const size_t smem = step_smem(H);
   if (kind == STEP_F) {
-    k_step<STEP_F><<<grid, kThreads, 0, st>>>(M, a);
+    k_step<STEP_F><<<grid, kStepThreads, 0, st>>>(M, a);
   } else {
     if (smem > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_step<STEP_FT><<<grid, kThreads, smem, st>>>(M, a);
+    k_step<STEP_FT><<<grid, kStepThreads, smem, st>>>(M, a);
   }
   QG_LAUNCHED();
 }
