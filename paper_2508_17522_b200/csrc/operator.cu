@@ -553,12 +553,17 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
   const unsigned grid = (unsigned)(H.nxu() + H.nyu());
   if (grid == 0) return;
   const size_t smem = step_smem(H);
+  static int threads = 0;
+  if (!threads) {  // QG_STEP_THREADS: A/B switch for the CTA size (32..128)
+    const char *e = std::getenv("QG_STEP_THREADS");
+    threads = e ? std::max(32, std::min(kStepThreads, std::atoi(e))) : kStepThreads;
+  }
   if (kind == STEP_F) {
-    k_step<STEP_F><<<grid, kStepThreads, 0, st>>>(M, a);
+    k_step<STEP_F><<<grid, threads, 0, st>>>(M, a);
   } else {
     if (smem > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_step<STEP_FT><<<grid, kStepThreads, smem, st>>>(M, a);
+    k_step<STEP_FT><<<grid, threads, smem, st>>>(M, a);
   }
   QG_LAUNCHED();
 }
