@@ -358,12 +358,23 @@ def cpu_sample_size(args, scaling, cores):
     return cores if scaling == "strong" else 1
 
 
+EXTRAPOLATE = {"c3": 4, "c4": 6, "c5b": 3}   # single-problem configs whose K=100 CPU eval takes minutes
+
+
 def cpu_baseline(bt, dirs, K, args, scaling):
     """The oracle (the reference algorithm restated) on the host cores."""
     from oracle import cpu_bench
 
     cores = cpu_bench.host_cores()
     nprob = bt.B
+    if args.config in EXTRAPOLATE:
+        ks = EXTRAPOLATE[args.config]
+        est, t0, per_iter = cpu_bench.extrapolated_eval_seconds(bt, dirs, 0, K, ks)
+        return {"value": round(1.0 / est, 6), "unit": "evals/s", "cores": 1, "kind": "port",
+                "sample": f"1 problem, jvp+vjp timed at caps 0 and {ks} (setup {t0:.2f} s, "
+                          f"{per_iter:.3f} s per LSMR iteration of jvp+vjp) extrapolated to K={K}; "
+                          f"1 process x 1 thread ({cpu_bench.cpu_model()})",
+                "seconds": round(est, 2)}
     sample = min(cpu_sample_size(args, scaling, cores), nprob)
     workers = min(cores, sample)
     secs = cpu_bench.time_sample(bt, dirs, K, range(sample), workers)

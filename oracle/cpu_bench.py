@@ -73,6 +73,21 @@ def time_sample(batch, dirs, K, problems, workers):
         return time.perf_counter() - t
 
 
+def extrapolated_eval_seconds(batch, dirs, p, K, k_small):
+    """Seconds of one jvp+vjp at cap K for problem p, estimated from runs at
+    caps 0 (setup only) and k_small: t(K) = t0 + K (t_k - t0) / k_small.
+    Used for configurations whose full-K CPU eval takes minutes."""
+    prob = problem(batch, dirs, p)
+    t = time.perf_counter()
+    eval_one(*prob, 0)
+    t0 = time.perf_counter() - t
+    t = time.perf_counter()
+    eval_one(*prob, k_small)
+    tk = time.perf_counter() - t
+    per_iter = max(tk - t0, 0.0) / k_small
+    return t0 + K * per_iter, t0, per_iter
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
