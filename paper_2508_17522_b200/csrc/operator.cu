@@ -39,7 +39,8 @@ template <class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
-                                         const double *v2, const double *x1, const double *x2, RowFn row) {
+                                         const double *v2, const double *x1, const double *x2, int G,
+                                         RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
     // warps claim pairs of slices dynamically (balances uneven units)
@@ -61,13 +62,17 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       if (rb >= 0) row(rb, b1, b2);
     }
   } else {
-    const int G = 32;
-    for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
-      double s1 = row_dot(rp1, c1, v1, x1, r, lane, G);
-      double s2 = rp2 ? row_dot(rp2, c2, v2, x2, r, lane, G) : 0.0;
+    // G lanes per CSR row (G from the average row length of the matrices),
+    // loops warp-uniform so every lane reaches the shuffles
+    const int lg = lane & (G - 1), gpw = 32 / G, nw = (int)(blockDim.x >> 5);
+    for (int base = u.row0 + warp * gpw; base < u.row1; base += nw * gpw) {
+      const int r = base + lane / G;
+      const bool valid = r < u.row1;
+      double s1 = valid ? row_dot(rp1, c1, v1, x1, r, lg, G) : 0.0;
+      double s2 = (valid && rp2) ? row_dot(rp2, c2, v2, x2, r, lg, G) : 0.0;
       s1 = gsum(s1, G);
       s2 = gsum(s2, G);
-      if (lane == 0) row(r, s1, s2);
+      if (valid && lg == 0) row(r, s1, s2);
     }
   }
 }
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
 
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
-    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2,
+    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, M.gx,
              [&](int r, double s1, double s2) {
                const double w = inX[r];
                double res;
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
                  const double o2 = (-s) + wN * M.b[r];
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
                });
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr,
+      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
                [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
       __syncthreads();
       // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step

@@ -18,6 +18,7 @@
 namespace qg {
 
 constexpr int kSellMaxRow = 256;
+constexpr int64_t kMinSellSlices = 148 * 16;  // ~16 warps of slices per SM
 
 void SellMat::release() {
   dev_free(off);
@@ -137,11 +138,10 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
 // the slice metadata and the padded matrices.  Returns the number of slices.
 int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const std::vector<int32_t> &rp1,
                    const std::vector<int32_t> *rp2, const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2,
-                   int32_t **rowof_out, cudaStream_t st) {
+                   int32_t **rowof_out, bool allow_sell, cudaStream_t st) {
   std::vector<int32_t> slice_pos, slice_n;
   int64_t ns = 0;
-  int max_row = kSellMaxRow;
-  if (const char *e = std::getenv("QG_SELL_MAX_ROW")) max_row = std::atoi(e);  // A/B switch (diagnostics)
+  const int max_row = allow_sell ? kSellMaxRow : -1;
   for (auto &u : units) {
     int maxlen = 0;
     for (int r = u.row0; r < u.row1; ++r) {
@@ -230,23 +230,21 @@ void build_tasks(Handle &H, cudaStream_t st) {
 
 void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
                 const std::vector<int32_t> &rpA, cudaStream_t st) {
-  const char *side = std::getenv("QG_SELL_SIDE");  // diagnostics: "x" or "y" only
-  const std::string keep = side ? side : "xy";
-  const char *saved = std::getenv("QG_SELL_MAX_ROW");
-  std::string saved_s = saved ? saved : "";
-  auto with_side = [&](bool on) {
-    if (on) {
-      if (saved) setenv("QG_SELL_MAX_ROW", saved_s.c_str(), 1); else unsetenv("QG_SELL_MAX_ROW");
-    } else {
-      setenv("QG_SELL_MAX_ROW", "-1", 1);
-    }
+  // Thread-per-row SELL pays off when a side has many short rows: enough
+  // slices to fill the GPU with warps and rows short enough that a thread's
+  // serial chain stays short.  Otherwise the side keeps G-lanes-per-row CSR
+  // (small single problems, long rows).  QG_SELL=0/1 forces (A/B testing).
+  const char *force = std::getenv("QG_SELL");
+  auto sell_ok = [&](int64_t rows, int64_t nnz) {
+    if (force) return std::atoi(force) != 0;
+    const double avg = rows ? (double)nnz / rows : 0.0;
+    return rows / 32 >= kMinSellSlices && avg <= 64.0;
   };
-  with_side(keep.find('x') != std::string::npos);
-  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, st);
-  with_side(keep.find('y') != std::string::npos);
+  const bool sx = sell_ok(H.NX, (int64_t)rpP[H.NX] + rpAT[H.NX]);
+  const bool sy = sell_ok(H.NY, (int64_t)rpA[H.NY]);
+  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
-                          &H.y_rowof, st);
-  with_side(true);
+                          &H.y_rowof, sy, st);
 }
 
 }  // namespace qg
