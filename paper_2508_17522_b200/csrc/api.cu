@@ -163,9 +163,11 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   H.gy = pick_group(nnzY, H.NY);
   // aim for >= 4 CTAs per SM when the batch is large enough, 2k..16k entries per unit
   const int64_t total = nnzX + nnzY + H.NX + H.NY;
-  int64_t target_nnz = std::max<int64_t>(2048, std::min<int64_t>(16384, total / (4 * 148) + 1));
+  // small problems get small units (all SMs busy, short per-warp chains),
+  // large batches amortise per-CTA work over up to 16k entries
+  int64_t target_nnz = std::max<int64_t>(256, std::min<int64_t>(16384, total / (8 * 148) + 1));
   const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
-  const int64_t target_rows_y = std::max<int64_t>(32, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
+  const int64_t target_rows_y = std::max<int64_t>(8, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
 
   // X units: nnz-balanced row ranges within each problem
   H.xunit_ptr.assign(B + 1, 0);

@@ -166,7 +166,7 @@ size_t ConeTable::psd_smem_prep() const {
 
 size_t ConeTable::psd_smem_apply() const {
   const int d = max_psd_order;
-  return (size_t)4 * d * d * sizeof(double);
+  return (size_t)4 * d * (d + 1) * sizeof(double);
 }
 
 void ConeTable::prepare(const double *z, double *proj, int dual_mode, bool want_deriv, cudaStream_t st) {

@@ -47,52 +47,63 @@ __device__ __forceinline__ void soc_apply_warp(const double *zb, int dim, double
   }
 }
 
-// PSD applier (cones.py:791-793): out = svec(V (B o (V' smat(in) V)) V').
-// CTA-wide; smem holds 4 order^2 doubles.  V, B column-major in global.
+// d x d product C = sum_k a(i,k) b(k,j), 2x2 register tiles per thread
+// (halves shared-memory traffic per FMA); out(i, j, c) stores.
+template <class FA, class FB, class FO>
+__device__ __forceinline__ void mm_tiles(int d, FA a, FB b, FO out) {
+  const int nt = (d + 1) / 2;
+  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
+    const int i0 = 2 * (t % nt), j0 = 2 * (t / nt);
+    const bool i1 = i0 + 1 < d, j1 = j0 + 1 < d;
+    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double a0 = a(i0, k), a1 = i1 ? a(i0 + 1, k) : 0.0;
+      const double b0 = b(k, j0), b1 = j1 ? b(k, j0 + 1) : 0.0;
+      c00 += a0 * b0;
+      c10 += a1 * b0;
+      c01 += a0 * b1;
+      c11 += a1 * b1;
+    }
+    out(i0, j0, c00);
+    if (i1) out(i0 + 1, j0, c10);
+    if (j1) out(i0, j0 + 1, c01);
+    if (i1 && j1) out(i0 + 1, j0 + 1, c11);
+  }
+}
+
+// PSD applier (cones.py:791-793): out = svec(V (B o (V' smat(in) V)) V'),
+// evaluated as V' (S V).  CTA-wide; smem holds 4 padded (d x (d+1))
+// matrices (leading dimension d+1 breaks the column-stride bank conflicts).
+// V, B column-major (d x d) in global.
 static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
-                              double *sm) {
-  double *V = sm, *S = sm + d * d, *T = sm + 2 * d * d, *W = sm + 3 * d * d;
-  const int dd = d * d;
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
-    V[idx] = Vg[idx];
-    const int i = idx % d, j = idx / d;  // S column major: S[i + j d]
+                                     double *sm) {
+  const int ld = d + 1, sz = d * ld;
+  double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = sm + 3 * sz;
+  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
+    const int i = idx % d, j = idx / d;
+    V[i + j * ld] = Vg[idx];
     const int a = i >= j ? i : j, b = i >= j ? j : i;
     const double v = in[svec_index(a, b, d)];
-    S[idx] = (a == b) ? v : v / kSqrt2;
+    S[i + j * ld] = (a == b) ? v : v / kSqrt2;
   }
   __syncthreads();
-  // T = V' S   (T[i,j] = sum_k V[k,i] S[k,j])
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
-    const int i = idx % d, j = idx / d;
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) s += V[k + i * d] * S[k + j * d];
-    T[idx] = s;
-  }
+  // T = S V
+  mm_tiles(d, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
+           [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
-  // W = (T V) o B
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
-    const int i = idx % d, j = idx / d;
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) s += T[i + k * d] * V[k + j * d];
-    W[idx] = Bg[idx] * s;
-  }
+  // W = (V' T) o B
+  mm_tiles(d, [&](int i, int k) { return V[k + i * ld]; }, [&](int k, int j) { return T[k + j * ld]; },
+           [&](int i, int j, double c) { W[i + j * ld] = Bg[i + j * d] * c; });
   __syncthreads();
   // T = V W
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
-    const int i = idx % d, j = idx / d;
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) s += V[i + k * d] * W[k + j * d];
-    T[idx] = s;
-  }
+  mm_tiles(d, [&](int i, int k) { return V[i + k * ld]; }, [&](int k, int j) { return W[k + j * ld]; },
+           [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
-  // out = svec(T V')
-  for (int idx = threadIdx.x; idx < dd; idx += blockDim.x) {
-    const int i = idx % d, j = idx / d;
-    if (i < j) continue;
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) s += T[i + k * d] * V[j + k * d];
-    out[svec_index(i, j, d)] = (i == j) ? s : s * kSqrt2;
-  }
+  // out = svec(T V') on the lower triangle
+  mm_tiles(d, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
+           [&](int i, int j, double c) {
+             if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
+           });
   __syncthreads();
 }
 
