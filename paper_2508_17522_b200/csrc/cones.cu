@@ -185,12 +185,15 @@ void ConeTable::prepare(const double *z, double *proj, int dual_mode, bool want_
 }
 
 void ConeTable::check_errors(cudaStream_t st) {
+  if (units.empty()) return;  // nothing was prepared (empty cone)
   unsigned long long key = 0;
   QG_CUDA(cudaMemcpyAsync(&key, d_err, sizeof(key), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
   if (key == ~0ull) return;
   const int code = (int)(key & 0xf);
   const long long blk = (long long)((key >> 4) & ((1ull << 56) - 1));
+  if (blk < 0 || blk >= (long long)h_blk.size())
+    throw Error{QG_ERR_CUDA, "corrupt cone error record (block " + std::to_string(blk) + ")"};
   const BlockInfo &b = h_blk[blk];
   static const char *names[] = {"zero", "nonneg", "soc", "psd", "exp", "dexp", "pow", "dpow"};
   std::string what;
@@ -302,6 +305,7 @@ void ConeTable::build(const std::vector<std::vector<qg_cone_block>> &per_prob, c
   d_tri_D = dev_alloc<double>(9 * ntri);
   d_tri_flip = dev_alloc<int32_t>(ntri);
   d_err = dev_alloc<unsigned long long>(1);
+  QG_CUDA(cudaMemsetAsync(d_err, 0xff, sizeof(unsigned long long), st));
   QG_CUDA(cudaStreamSynchronize(st));  // host vectors above are sources of async copies
 }
 
