@@ -161,6 +161,18 @@ def to_dev(a, dtype):
     return t.to(device=device(), dtype=dtype, non_blocking=False).contiguous()
 
 
+def to_host(t):
+    """CUDA tensor -> NumPy array through a pinned staging buffer (torch's
+    caching host allocator reuses it across calls; DMA instead of a pageable
+    copy)."""
+    import torch
+
+    out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    out.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return out.numpy()
+
+
 def empty(n, dtype=None):
     import torch
 

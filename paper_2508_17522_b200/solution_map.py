@@ -196,14 +196,14 @@ class QCPBatch:
 
         d = [N.to_dev(a, torch.float64) for a in (dP, dA, dq, db)]
         dx, dy, ds, diags = self.jvp_device(*d, **kw)
-        return dx.cpu().numpy(), dy.cpu().numpy(), ds.cpu().numpy(), [_diag(g) for g in diags]
+        return N.to_host(dx), N.to_host(dy), N.to_host(ds), [_diag(g) for g in diags]
 
     def vjp_host(self, dx, dy, ds, **kw):
         import torch
 
         d = [N.to_dev(a, torch.float64) for a in (dx, dy, ds)]
         dP, dA, dq, db, diags = self.vjp_device(*d, **kw)
-        return (dP.cpu().numpy(), dA.cpu().numpy(), dq.cpu().numpy(), db.cpu().numpy(),
+        return (N.to_host(dP), N.to_host(dA), N.to_host(dq), N.to_host(db),
                 [_diag(g) for g in diags])
 
     def time_kernel(self, which, reps=20):
@@ -323,7 +323,7 @@ class QCPBatch:
             args["dA_struct"] = (i64([d.dA.col_ptr for d in dthetas]), i64([d.dA.row_idx for d in dthetas]),
                                  [d.dA.nnz for d in dthetas])
         dx, dy, ds, diags = self.jvp_device(**args, **kw)
-        dx, dy, ds = dx.cpu().numpy(), dy.cpu().numpy(), ds.cpu().numpy()
+        dx, dy, ds = N.to_host(dx), N.to_host(dy), N.to_host(ds)
         out = []
         for i in range(self.B):
             xs, ys = slice(self.xoff[i], self.xoff[i + 1]), slice(self.yoff[i], self.yoff[i + 1])
@@ -336,7 +336,7 @@ class QCPBatch:
         cat = lambda xs: N.to_dev(np.concatenate(xs) if xs else np.zeros(0), torch.float64)
         dP, dA, dq, db, diags = self.vjp_device(cat([d.dx for d in deltas]), cat([d.dy for d in deltas]),
                                                 cat([d.ds for d in deltas]), **kw)
-        dP, dA, dq, db = (t.cpu().numpy() for t in (dP, dA, dq, db))
+        dP, dA, dq, db = (N.to_host(t) for t in (dP, dA, dq, db))
         out = []
         for i, th in enumerate(self.thetas):
             g = DataPerturbation(th.P.with_values(dP[self.poff[i]:self.poff[i + 1]]),
