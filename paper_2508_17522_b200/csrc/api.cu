@@ -203,6 +203,10 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   build_sell(H, rpP, rpAT, rpA, st);
   build_tasks(H, st);
   trace("sell layout");
+  H.d_xoff = dev_alloc<int64_t>(B + 1);
+  H.d_yoff = dev_alloc<int64_t>(B + 1);
+  QG_CUDA(cudaMemcpyAsync(H.d_xoff, H.xoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+  QG_CUDA(cudaMemcpyAsync(H.d_yoff, H.yoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
   H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
   H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xunit_ptr, H.xunit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));

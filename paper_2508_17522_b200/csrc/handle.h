@@ -49,8 +49,9 @@ struct SellMat {
   int32_t *w = nullptr;
   int32_t *col = nullptr;
   double *val = nullptr;
+  uint16_t *col16 = nullptr;
   int64_t entries = 0;
-  SellView view() const { return SellView{off, w, col, val}; }
+  SellView view() const { return SellView{off, w, col, val, col16}; }
   void release();
 };
 

@@ -40,7 +40,7 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
                                          const double *v2, const double *x1, const double *x2, int G,
-                                         RowFn row) {
+                                         int64_t b1, int64_t b2, RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
     // warps claim pairs of slices dynamically (balances uneven units)
@@ -55,11 +55,11 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       const int sb = s + 1 < u.s1 ? s + 1 : -1;
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
-      double a1, b1, a2 = 0.0, b2 = 0.0;
-      sell_dot2(S1, s, sb, lane, x1, a1, b1);
-      if (S2) sell_dot2(*S2, s, sb, lane, x2, a2, b2);
+      double a1, b1v, a2 = 0.0, b2v = 0.0;
+      sell_dot2(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
+      if (S2) sell_dot2(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
       if (ra >= 0) row(ra, a1, a2);
-      if (rb >= 0) row(rb, b1, b2);
+      if (rb >= 0) row(rb, b1v, b2v);
     }
   } else {
     // G lanes per CSR row (G from the average row length of the matrices),
@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, M.gx,
+             M.xoff[p], M.yoff[p],
              [&](int r, double s1, double s2) {
                const double w = inX[r];
                double res;
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
       for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
+               M.xoff[p], 0,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
                  const double o2 = (-s) + wN * M.b[r];
@@ -188,6 +190,7 @@ __global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
       for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
+               M.xoff[p], 0,
                [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
       __syncthreads();
       // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step
@@ -545,6 +548,7 @@ Mats make_mats(const Handle &H) {
   M.dpi = H.cones.view();
   M.sP = H.sP.view(); M.sAT = H.sAT.view(); M.sA = H.sA.view();
   M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
+  M.xoff = H.d_xoff; M.yoff = H.d_yoff;
   M.tasks = H.d_tasks; M.ntx = H.ntx; M.nty = H.nty;
   M.xt_ptr = H.d_xt_ptr; M.yt_ptr = H.d_yt_ptr;
   M.part_t = H.ws.part_t;

@@ -20,6 +20,7 @@ struct Mats {
   DpiView dpi;
   SellView sP, sAT, sA;                 // SELL copies (MODE_SELL units)
   const int32_t *x_rowof, *y_rowof;     // lane -> row per slice (-1 = padding)
+  const int64_t *xoff, *yoff;           // [B+1] problem offsets in X / Y
   const Task *tasks;                    // warp tasks: X [0, ntx), Y [ntx, ntx + nty)
   int64_t ntx, nty;
   const int64_t *xt_ptr, *yt_ptr;       // [B+1] task ranges per problem
@@ -27,24 +28,24 @@ struct Mats {
   double *part_u;                       // per-unit partial sums (X units then Y units)
 };
 
-// Row sum of one SELL slice lane: sum_k val * vec[col] in storage order.
-__device__ __forceinline__ double sell_dot(const SellView &S, int64_t s, int lane, const double *vec) {
-  const int64_t o = S.off[s] + lane;
-  const int w = S.w[s];
-  double acc = 0.0;
-#pragma unroll 4
-  for (int k = 0; k < w; ++k) {
-    const int64_t p = o + 32LL * k;
-    acc += __ldcs(S.val + p) * vec[__ldcs(S.col + p)];
-  }
-  return acc;
-}
-
 // Two slices of one matrix at once (independent load streams -> twice the
 // memory-level parallelism per warp); slice b may be absent (sb < 0).  Each
 // lane's sums stay in storage order.
+template <class Idx>
+__device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *col, int64_t sa, int64_t sb, int lane,
+                                            const double *vec, double &acc_a, double &acc_b);
+
+// Dispatch on the index width: 16-bit problem-local indices gather from
+// vec_local (= vec + this problem's column base), 32-bit global ones from vec.
 __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t sb, int lane, const double *vec,
-                                          double &acc_a, double &acc_b) {
+                                          const double *vec_local, double &acc_a, double &acc_b) {
+  if (S.col16) sell_dot2_t(S, S.col16, sa, sb, lane, vec_local, acc_a, acc_b);
+  else sell_dot2_t(S, S.col, sa, sb, lane, vec, acc_a, acc_b);
+}
+
+template <class Idx>
+__device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, int64_t sa, int64_t sb, int lane,
+                                            const double *vec, double &acc_a, double &acc_b) {
   const int64_t oa = S.off[sa] + lane;
   const int wa = S.w[sa];
   const int64_t ob = sb >= 0 ? S.off[sb] + lane : 0;
@@ -56,19 +57,19 @@ __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t
   for (; k < wm; ++k) {
     const int64_t pa = oa + 32LL * k, pb = ob + 32LL * k;
     const double va = __ldcs(S.val + pa), vb = __ldcs(S.val + pb);
-    const int ca = __ldcs(S.col + pa), cb = __ldcs(S.col + pb);
+    const int ca = __ldcs(colp + pa), cb = __ldcs(colp + pb);
     a += va * vec[ca];
     b += vb * vec[cb];
   }
 #pragma unroll 4
   for (int j = k; j < wa; ++j) {
     const int64_t pa = oa + 32LL * j;
-    a += __ldcs(S.val + pa) * vec[__ldcs(S.col + pa)];
+    a += __ldcs(S.val + pa) * vec[__ldcs(colp + pa)];
   }
 #pragma unroll 4
   for (int j = k; j < wb; ++j) {
     const int64_t pb = ob + 32LL * j;
-    b += __ldcs(S.val + pb) * vec[__ldcs(S.col + pb)];
+    b += __ldcs(S.val + pb) * vec[__ldcs(colp + pb)];
   }
   acc_a = a;
   acc_b = b;

@@ -107,8 +107,10 @@ struct Task {
 struct SellView {
   const int64_t *off;   // [nslices] first entry of the slice
   const int32_t *w;     // [nslices] slice width (longest row)
-  const int32_t *col;   // padded entries: col 0, val 0
+  const int32_t *col;   // padded entries: col 0, val 0 (global column index)
   const double *val;
+  const uint16_t *col16;  // problem-local column index (null unless every problem
+                          // has < 65536 columns): 10 instead of 12 B per entry
 };
 
 struct Csr {

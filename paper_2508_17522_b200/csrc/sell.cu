@@ -25,6 +25,8 @@ void SellMat::release() {
   dev_free(w);
   dev_free(col);
   dev_free(val);
+  dev_free(col16);
+  col16 = nullptr;
   off = nullptr;
   w = nullptr;
   col = nullptr;
@@ -78,8 +80,10 @@ __global__ void k_width32(const int32_t *w, int64_t n, int64_t *out) {
 }
 
 // warp per slice: scatter the CSR rows into the slice layout
+// col16 (when non-null) receives col - cbase[slice] (problem-local index).
 __global__ void k_sell_fill(int64_t nslices, const int32_t *rowof, const int32_t *rp, const int32_t *csr_col,
-                            const double *csr_val, const int64_t *off, const int32_t *w, int32_t *col, double *val) {
+                            const double *csr_val, const int64_t *off, const int32_t *w, int32_t *col, double *val,
+                            uint16_t *col16, const int32_t *cbase) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;
@@ -87,22 +91,20 @@ __global__ void k_sell_fill(int64_t nslices, const int32_t *rowof, const int32_t
   const int k0 = r >= 0 ? rp[r] : 0, len = r >= 0 ? rp[r + 1] - k0 : 0;
   const int64_t o = off[s];
   const int width = w[s];
+  const int base = col16 ? cbase[s] : 0;
   for (int k = 0; k < width; ++k) {
     const int64_t pos = o + 32LL * k + lane;
-    if (k < len) {
-      col[pos] = csr_col[k0 + k];
-      val[pos] = csr_val[k0 + k];
-    } else {
-      col[pos] = 0;
-      val[pos] = 0.0;
-    }
+    const bool in = k < len;
+    val[pos] = in ? csr_val[k0 + k] : 0.0;
+    if (col16) col16[pos] = in ? (uint16_t)(csr_col[k0 + k] - base) : (uint16_t)0;
+    else col[pos] = in ? csr_col[k0 + k] : 0;
   }
 }
 
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_t *wsrc, const DevCsr &csr,
-                 cudaStream_t st) {
+                 const int32_t *d_cbase, cudaStream_t st) {
   M.w = dev_alloc<int32_t>(nslices);
   QG_CUDA(cudaMemcpyAsync(M.w, wsrc, sizeof(int32_t) * nslices, cudaMemcpyDeviceToDevice, st));
   int64_t *w32 = dev_alloc<int64_t>(nslices);
@@ -122,11 +124,12 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
   QG_CUDA(cudaMemcpyAsync(&total, M.off + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
   M.entries = total;
-  M.col = dev_alloc<int32_t>(total);
+  if (d_cbase) M.col16 = dev_alloc<uint16_t>(total);
+  else M.col = dev_alloc<int32_t>(total);
   M.val = dev_alloc<double>(total);
   if (total > 0) {
     k_sell_fill<<<nb(nslices * 32), 256, 0, st>>>(nslices, rowof, csr.rp, csr.col, csr.val, M.off, M.w, M.col,
-                                                  M.val);
+                                                  M.val, M.col16, d_cbase);
     QG_LAUNCHED();
   }
   dev_free(tmp);
@@ -136,10 +139,13 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
 
 // Decide modes and slice ranges on the host, sort rows on the device, build
 // the slice metadata and the padded matrices.  Returns the number of slices.
+// cb1 / cb2: per-problem column base of matrix 1 / 2 (X or Y offsets) when
+// 16-bit local indices are used, else null.
 int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const std::vector<int32_t> &rp1,
                    const std::vector<int32_t> *rp2, const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2,
-                   int32_t **rowof_out, bool allow_sell, cudaStream_t st) {
-  std::vector<int32_t> slice_pos, slice_n;
+                   int32_t **rowof_out, bool allow_sell, const std::vector<int64_t> *cb1,
+                   const std::vector<int64_t> *cb2, cudaStream_t st) {
+  std::vector<int32_t> slice_pos, slice_n, slice_b1, slice_b2;
   int64_t ns = 0;
   const int max_row = allow_sell ? kSellMaxRow : -1;
   for (auto &u : units) {
@@ -155,6 +161,8 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
       for (int r = u.row0; r < u.row1; r += 32) {
         slice_pos.push_back(r);
         slice_n.push_back(std::min(32, u.row1 - r));
+        if (cb1) slice_b1.push_back((int32_t)(*cb1)[u.prob]);
+        if (cb2) slice_b2.push_back((int32_t)(*cb2)[u.prob]);
       }
       ns += (u.row1 - u.row0 + 31) / 32;
       u.s1 = (int32_t)ns;
@@ -185,11 +193,20 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
   Lens L1{m1.rp, m2 ? m2->rp : nullptr};
   k_slice_meta<<<nb(ns * 32), 256, 0, st>>>(d_pos, d_n, ns, rows_s, L1, *rowof_out, w1, w2);
   QG_LAUNCHED();
-  fill_matrix(s1, ns, *rowof_out, w1, m1, st);
-  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, st);
+  int32_t *d_b1 = nullptr, *d_b2 = nullptr;
+  if (cb1) {
+    d_b1 = dev_alloc<int32_t>(ns);
+    QG_CUDA(cudaMemcpyAsync(d_b1, slice_b1.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
+  }
+  if (cb2) {
+    d_b2 = dev_alloc<int32_t>(ns);
+    QG_CUDA(cudaMemcpyAsync(d_b2, slice_b2.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
+  }
+  fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, st);
+  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, st);
   QG_CUDA(cudaStreamSynchronize(st));
   dev_free(keys); dev_free(keys_s); dev_free(rows); dev_free(rows_s); dev_free(tmp);
-  dev_free(d_pos); dev_free(d_n); dev_free(w1); dev_free(w2);
+  dev_free(d_pos); dev_free(d_n); dev_free(w1); dev_free(w2); dev_free(d_b1); dev_free(d_b2);
   return ns;
 }
 
@@ -242,9 +259,15 @@ void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<in
   };
   const bool sx = sell_ok(H.NX, (int64_t)rpP[H.NX] + rpAT[H.NX]);
   const bool sy = sell_ok(H.NY, (int64_t)rpA[H.NY]);
-  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx, st);
+  // 16-bit problem-local column indices when every problem is small enough
+  const char *f16 = std::getenv("QG_SELL16");
+  bool small = f16 ? std::atoi(f16) != 0 : true;
+  for (int p = 0; p < H.B && small; ++p) small = H.n[p] < 65536 && H.m[p] < 65536;
+  const auto *bx = small ? &H.xoff : nullptr, *by = small ? &H.yoff : nullptr;
+  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,
+                          bx, by, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
-                          &H.y_rowof, sy, st);
+                          &H.y_rowof, sy, bx, nullptr, st);
 }
 
 }  // namespace qg
