@@ -120,8 +120,8 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
 // closing reduction) at the same register-limited occupancy (8 CTAs/SM).
 constexpr int kStepThreads = 128;
 
-template <int KIND>
-__global__ void __launch_bounds__(kStepThreads, 8) k_step(Mats M, StepArgs a) {
+template <int KIND, int MINB>
+__global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
   const bool isx = (int)blockIdx.x < M.nxu;
@@ -567,12 +567,20 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
     const char *e = std::getenv("QG_STEP_THREADS");
     threads = e ? std::max(32, std::min(kStepThreads, std::atoi(e))) : kStepThreads;
   }
+  static int minb = 0;
+  if (!minb) {  // QG_STEP_MINB: A/B switch for the occupancy target (register cap)
+    const char *e = std::getenv("QG_STEP_MINB");
+    minb = (e && std::atoi(e) >= 12) ? 12 : 8;
+  }
+  auto go = [&](auto kern, size_t sm_bytes) {
+    if (sm_bytes > 48 * 1024)
+      QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
+    kern<<<grid, threads, sm_bytes, st>>>(M, a);
+  };
   if (kind == STEP_F) {
-    k_step<STEP_F><<<grid, threads, 0, st>>>(M, a);
+    if (minb == 12) go(k_step<STEP_F, 12>, 0); else go(k_step<STEP_F, 8>, 0);
   } else {
-    if (smem > 48 * 1024)
-      QG_CUDA(cudaFuncSetAttribute(k_step<STEP_FT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_step<STEP_FT><<<grid, threads, smem, st>>>(M, a);
+    if (minb == 12) go(k_step<STEP_FT, 12>, smem); else go(k_step<STEP_FT, 8>, smem);
   }
   QG_LAUNCHED();
 }
