@@ -567,11 +567,11 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
     const char *e = std::getenv("QG_STEP_THREADS");
     threads = e ? std::max(32, std::min(kStepThreads, std::atoi(e))) : kStepThreads;
   }
-  static int minb = 0;
-  if (!minb) {  // QG_STEP_MINB: A/B switch for the occupancy target (register cap)
-    const char *e = std::getenv("QG_STEP_MINB");
-    minb = (e && std::atoi(e) >= 12) ? 12 : 8;
-  }
+  // Occupancy target: SELL loops keep many loads in flight per thread (64
+  // registers, 8 CTAs/SM measured best); the CSR group path gains from 12
+  // CTAs/SM (c3: 11.2 -> 8.7 ms per jvp).  QG_STEP_MINB=8|12 overrides.
+  static const char *env_minb = std::getenv("QG_STEP_MINB");
+  const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (H.nslice_x + H.nslice_y > 0 ? 8 : 12);
   auto go = [&](auto kern, size_t sm_bytes) {
     if (sm_bytes > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
