@@ -268,6 +268,7 @@ def run_ours(args):
         outs = {}
 
         def step_host():
+            outs.clear()  # release last step's pinned result buffers back to torch's host cache
             b = QCPBatch.from_host(*sizes, pin)
             outs["j"] = b.jvp_host(pdir["dP"], pdir["dA"], pdir["dq"], pdir["db"], **kw)
             outs["v"] = b.vjp_host(pdir["dx"], pdir["dy"], pdir["ds"], **kw)
@@ -290,7 +291,9 @@ def run_ours(args):
     t_f = b.time_kernel(0, reps=20)
     peaks = _peaks()
     ach = ab["FT"] / (t_ft / 1e3) / 1e9
-    roof = {"kernel": "k_step<FT> (CSR SpMV A,A',P + D Pi x2 epilogue)", "bound": "hbm",
+    sx, sy = b.layout()
+    spmv = "SELL-32" if sx and sy else ("SELL-32/CSR" if sx or sy else "CSR group-per-row")
+    roof = {"kernel": f"k_step<FT> ({spmv} SpMV A,A',P + D Pi x2 epilogue)", "bound": "hbm",
             "achieved": round(ach, 1), "peak": peaks[0], "peak_source": peaks[1], "unit": "GB/s",
             "frac": round(ach / peaks[0], 4), "traffic": _traffic(args.config, ab["FT"]),
             "alg_bytes_per_launch": ab["FT"], "launch_ms": round(t_ft, 4),
@@ -352,10 +355,21 @@ def _traffic(cfg, alg):
 
 
 # --------------------------------------------------------- CPU reference --
-def cpu_sample_size(args, scaling, cores):
+def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=None):
+    """Problems in the CPU sample: ``--cpu-sample`` if given, else one per
+    core, grown (in whole rounds over the cores, up to the batch) until the
+    sample is about ``target_s`` seconds of CPU work."""
     if args.cpu_sample:
         return args.cpu_sample
-    return cores if scaling == "strong" else 1
+    base = cores if scaling == "strong" else 1
+    if target_s is None or bt is None or scaling != "strong":
+        return base
+    from oracle import cpu_bench
+
+    base = min(base, bt.B)
+    secs = cpu_bench.time_sample(bt, dirs, K, range(base), min(cores, base))
+    rounds = max(1, int(target_s / max(secs, 1e-3)))
+    return min(bt.B, base * rounds)
 
 
 EXTRAPOLATE = {"c3": 4, "c4": 6, "c5b": 3}   # single-problem configs whose K=100 CPU eval takes minutes
@@ -375,7 +389,7 @@ def cpu_baseline(bt, dirs, K, args, scaling):
                           f"{per_iter:.3f} s per LSMR iteration of jvp+vjp) extrapolated to K={K}; "
                           f"1 process x 1 thread ({cpu_bench.cpu_model()})",
                 "seconds": round(est, 2)}
-    sample = min(cpu_sample_size(args, scaling, cores), nprob)
+    sample = min(cpu_sample_size(args, scaling, cores, bt, dirs, K, target_s=12.0), nprob)
     workers = min(cores, sample)
     secs = cpu_bench.time_sample(bt, dirs, K, range(sample), workers)
     return {"value": round(sample / secs, 4), "unit": "evals/s", "cores": workers, "kind": "port",
@@ -393,7 +407,7 @@ def run_reference(args):
     bt, dirs, units_total, units_here, scaling = build_workload(args.config, 0, 1, args.batch)
     K = args.lsmr_iters
     cores = cpu_bench.host_cores()
-    sample = min(cpu_sample_size(args, scaling, cores), bt.B)
+    sample = min(cpu_sample_size(args, scaling, cores, bt, dirs, K, target_s=6.0), bt.B)
     workers = min(cores, sample)
     for _ in range(args.warmup):
         cpu_bench.time_sample(bt, dirs, K, range(sample), workers)

@@ -109,6 +109,10 @@ const char *qg_version(void);
 int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream);
 int qg_destroy(qg_handle *h);
 int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_t *total_m);
+/* SpMV layout chosen at create (diagnostic; no reference counterpart): number
+ * of SELL-32 slices on the X side (rows of P and A') and on the Y side (rows
+ * of A); 0 = that side runs the CSR group-per-row path. */
+int qg_handle_layout(const qg_handle *h, int64_t *sell_slices_x, int64_t *sell_slices_y);
 
 /* jvp: outputs dx (sum n), dy, ds (sum m), diag[nprob] (host). */
 int qg_jvp(qg_handle *h, const qg_perturbation *dtheta, const qg_lsmr_opts *opts,

@@ -68,6 +68,7 @@ _SIGS = {
     "qg_create_batch": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(BatchDesc), c_vp]),
     "qg_destroy": (ctypes.c_int, [c_vp]),
     "qg_handle_sizes": (ctypes.c_int, [c_vp, P_i64, P_i64, P_i64]),
+    "qg_handle_layout": (ctypes.c_int, [c_vp, P_i64, P_i64]),
     "qg_jvp": (ctypes.c_int, [c_vp, ctypes.POINTER(PerturbationC), ctypes.POINTER(LsmrOpts),
                               c_vp, c_vp, c_vp, ctypes.POINTER(DiagC), c_vp]),
     "qg_vjp": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(LsmrOpts),
@@ -155,7 +156,8 @@ def to_dev(a, dtype):
     import torch
 
     if isinstance(a, torch.Tensor):
-        return a.to(device=device(), dtype=dtype).contiguous()
+        # pinned sources DMA asynchronously, ordered on the current stream
+        return a.to(device=device(), dtype=dtype, non_blocking=a.is_pinned()).contiguous()
     arr = np.ascontiguousarray(a)
     t = torch.from_numpy(arr)
     return t.to(device=device(), dtype=dtype, non_blocking=False).contiguous()

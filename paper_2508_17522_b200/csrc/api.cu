@@ -487,6 +487,14 @@ int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_
   QG_API_END
 }
 
+int qg_handle_layout(const qg_handle *h, int64_t *sell_slices_x, int64_t *sell_slices_y) {
+  QG_API_BEGIN_NS
+  const Handle *H = reinterpret_cast<const Handle *>(h);
+  *sell_slices_x = H->nslice_x;
+  *sell_slices_y = H->nslice_y;
+  QG_API_END
+}
+
 int qg_embedding_point(qg_handle *h, double *pz, void *stream) {
   QG_API_BEGIN
   Handle &H = *reinterpret_cast<Handle *>(h);

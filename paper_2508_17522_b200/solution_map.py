@@ -206,6 +206,12 @@ class QCPBatch:
         return (N.to_host(dP), N.to_host(dA), N.to_host(dq), N.to_host(db),
                 [_diag(g) for g in diags])
 
+    def layout(self):
+        """(SELL-32 slices on the X side, on the Y side); 0 = CSR path."""
+        sx, sy = N.ctypes.c_int64(), N.ctypes.c_int64()
+        N.check(N.lib().qg_handle_layout(self._h, N.ctypes.byref(sx), N.ctypes.byref(sy)))
+        return int(sx.value), int(sy.value)
+
     def time_kernel(self, which, reps=20):
         """Mean device ms per launch of a hot kernel (0: F step, 1: F' step,
         2: LSMR update), CUDA events on the current stream."""
