@@ -15,11 +15,13 @@ outputs inside the timed region).
 Default workload (``--config c5a``): BASELINE configs[4], a batch of 4096
 independent QCPs (n=1000, m=1500 = nonneg(500) + 100 x SOC(10), nnz(A) =
 1.5e4 each), sharded over the ranks (strong scaling of a fixed batch).
-Single-problem configs (c1..c4, c5b) run as replicas at N > 1.
+``--config c5b`` at N > 1 splits the ONE LASSO problem by the rows of A
+over the ranks (dist.py; strong scaling; one NCCL sum-allreduce of the A'
+partials per operator step, inside the LSMR graphs).  The other
+single-problem configs (c1..c4) run as replicas at N > 1.
 
 Multi-GPU: launched by torch.distributed.run, one rank per GPU; device
-timing max-reduced over ranks (NCCL only for that and the barrier -- the
-batch path has no data-path collective).
+timing max-reduced over ranks (the batch path has no data-path collective).
 """
 
 import argparse
@@ -118,8 +120,34 @@ def build_workload(cfg, rank, world, batch_override=None):
         lo, hi = shard_range(total, rank, world)
         bt = synth.generate(cfg, seed=1000 + rank, batch=hi - lo)
         return bt, synth.directions(bt, seed=2000 + rank), total, hi - lo, "strong"
+    if cfg in PARTITIONED and world > 1:
+        # one problem, rows of A split over the ranks; every
+        # rank builds the same instance and keeps its rows
+        full = synth.generate(cfg, seed=1000)
+        bt, dirs = row_shard(full, synth.directions(full, seed=2000), rank, world)
+        return bt, dirs, 1, 1, "strong"
     bt = synth.generate(cfg, seed=1000 + rank)
     return bt, synth.directions(bt, seed=2000 + rank), world, 1, "weak"
+
+
+PARTITIONED = ("c5b",)   # single problems run row-partitioned at N > 1 (others: replicas)
+
+
+def row_shard(full, dirs, rank, world):
+    """This rank's row shard of a single-problem synth.Batch (and of its
+    directions) as a synth.Batch of the local problem; ``.shard`` keeps the
+    partition (dist.RowShard)."""
+    from paper_2508_17522_b200 import dist, synth
+
+    s = dist.make_shard(full, rank, world)
+    a = s.arrays
+    bt = synth.Batch(n=[s.n], m=[s.m], blocks=[s.blocks], P_colptr=a["P_colptr"], P_rowidx=a["P_rowidx"],
+                     P_vals=a["P_vals"], A_colptr=a["A_colptr"], A_rowidx=a["A_rowidx"], A_vals=a["A_vals"],
+                     q=a["q"], b=a["b"], x=a["x"], y=a["y"], s=a["s"], P_nnz=[s.P_nnz], A_nnz=[s.A_nnz])
+    bt.shard = s
+    d = synth.Directions(dP=dirs.dP, dA=dirs.dA[s.global_positions], dq=dirs.dq, db=dirs.db[s.lo:s.hi],
+                         dx=dirs.dx, dy=dirs.dy[s.lo:s.hi], ds=dirs.ds[s.lo:s.hi])
+    return bt, d
 
 
 def batch_bytes(bt):
@@ -223,9 +251,14 @@ def run_ours(args):
             for k in ("dP", "dA", "dq", "db", "dx", "dy", "ds")}
     sizes = (bt.n, bt.m, bt.P_nnz, bt.A_nnz, blocks)
     flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)
+    comm = None
+    if getattr(bt, "shard", None) is not None:
+        from paper_2508_17522_b200 import dist as qdist
+
+        comm = qdist.Comm.nccl()   # the row-partitioned exchange (NCCL inside the LSMR graphs)
 
     def step_device():
-        b = QCPBatch.from_device(*sizes, dev_in)
+        b = QCPBatch.from_device(*sizes, dev_in, comm=comm)
         b.jvp_device(ddir["dP"], ddir["dA"], ddir["dq"], ddir["db"], **kw)
         b.vjp_device(ddir["dx"], ddir["dy"], ddir["ds"], **kw)
         return b
@@ -269,7 +302,7 @@ def run_ours(args):
 
         def step_host():
             outs.clear()  # release last step's pinned result buffers back to torch's host cache
-            b = QCPBatch.from_host(*sizes, pin)
+            b = QCPBatch.from_host(*sizes, pin, comm=comm)
             outs["j"] = b.jvp_host(pdir["dP"], pdir["dA"], pdir["dq"], pdir["db"], **kw)
             outs["v"] = b.vjp_host(pdir["dx"], pdir["dy"], pdir["ds"], **kw)
             b.close()
@@ -301,7 +334,7 @@ def run_ours(args):
                        "alg_bytes_per_launch": ab["F"]}}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # contract: N=1 only
         cpu = cpu_baseline(bt, dirs, K, args, scaling)
     if rank == 0:
         line = {
@@ -313,7 +346,7 @@ def run_ours(args):
                        "per_rank_problems": units_here,
                        "lsmr": f"fixed cap K={K} (atol=btol=0) for jvp and vjp; step includes batch preparation",
                        "l2": "256 MiB L2 flush between timed steps (excluded from timing)",
-                       "parallelism": f"{'batch shards' if scaling == 'strong' else 'replicas'} x{world}"},
+                       "parallelism": (f"row shards of one problem x{world} (NCCL allreduce of the A' partials)" if comm else f"{'batch shards' if scaling == 'strong' else 'replicas'} x{world}")},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(), "lsmr_iterations_per_s": round(value * 2 * K, 1),
         }

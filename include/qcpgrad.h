@@ -155,6 +155,32 @@ int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stre
 /* Number of kernels this library launched since load (telemetry). */
 int64_t qg_kernel_launches(void);
 
+/* ---- row-partitioned mode (no reference counterpart:
+ * the reference is single-process).  The Y rows of A -- with b, y, s and
+ * whole cone blocks (zero / nonneg blocks may be cut anywhere) -- are split
+ * over ranks; every rank holds the full X side (P, q, x) and the T entry.
+ * Each rank creates a handle from ITS shard (qg_batch_desc with the local m,
+ * local A rows as CSC over all n columns, local b, y, s, blocks) plus a
+ * communicator; jvp / vjp then run the same LSMR on every rank with one
+ * sum-allreduce of the A' partials per operator step and one of the
+ * per-problem partial sums per finalize.  Outputs: dx, dq, dP replicated;
+ * dy, ds, db and dA (local rows, CSC order of the local A) per rank.
+ * qg_check is not available on a partitioned handle. */
+typedef struct qg_comm qg_comm;
+/* rank 0 creates the NCCL unique id and ships it to the others (any channel) */
+int qg_comm_nccl_id(unsigned char id[128]);
+/* one rank per GPU / process; NCCL resolved at run time from libnccl.so.2 */
+int qg_comm_create_nccl(qg_comm **out, const unsigned char id[128], int world, int rank);
+/* `world` (1..8) shards on the current device, one host thread per shard:
+ * out[r] is shard r's communicator.  Not graph-capturable (host barrier). */
+int qg_comm_create_local(qg_comm **out, int world);
+int qg_comm_destroy(qg_comm *c);
+int qg_comm_rank(const qg_comm *c, int *rank, int *world);
+/* in-place sum over ranks of n doubles (device buffer), synchronous */
+int qg_comm_allreduce(qg_comm *c, double *buf, int64_t n, void *stream);
+/* create a handle over this rank's shard; `comm` must outlive the handle */
+int qg_create_batch_dist(qg_handle **out, const qg_batch_desc *desc, qg_comm *comm, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,14 @@ _SIGS = {
     "qg_cones_apply": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp]),
     "qg_time_kernel": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(c_dbl), c_vp]),
     "qg_spmv_csc": (ctypes.c_int, [c_i64, c_i64, c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp]),
+    "qg_comm_nccl_id": (ctypes.c_int, [ctypes.POINTER(ctypes.c_ubyte)]),
+    "qg_comm_create_nccl": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(ctypes.c_ubyte), ctypes.c_int,
+                                           ctypes.c_int]),
+    "qg_comm_create_local": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.c_int]),
+    "qg_comm_destroy": (ctypes.c_int, [c_vp]),
+    "qg_comm_rank": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "qg_comm_allreduce": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp]),
+    "qg_create_batch_dist": (ctypes.c_int, [ctypes.POINTER(c_vp), ctypes.POINTER(BatchDesc), c_vp, c_vp]),
 }
 
 _lib = None

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib")
-SOURCES = ["api.cu", "operator.cu", "assembly.cu", "cones.cu", "transpose.cu", "sell.cu"]
+SOURCES = ["api.cu", "operator.cu", "assembly.cu", "cones.cu", "transpose.cu", "sell.cu", "comm.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
@@ -62,7 +62,7 @@ def build(verbose=False, force=False):
     lib = os.path.join(OUT, "libqcpgrad.so")
     if force or _newer(lib, objs):
         cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-cudart", "static",
-               "-o", lib] + objs
+               "-o", lib] + objs + ["-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

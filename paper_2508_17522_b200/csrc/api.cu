@@ -82,6 +82,7 @@ Handle::~Handle() {
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
   dev_free(d_tasks); dev_free(d_xt_ptr); dev_free(d_yt_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
+  dev_free(xred); dev_free(psum); dev_free(d_iota);
   ws.release();
   std::lock_guard<std::mutex> g(g_graph_mu);
   auto it = g_graphs.find(this);
@@ -237,6 +238,15 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
   W.h_nactive = nullptr;
+  if (H.comm) {
+    H.xred = dev_alloc<double>(H.NX);
+    H.psum = dev_alloc<double>(2 * (size_t)B * kSlots);
+    std::vector<int64_t> iota(B + 1);
+    for (int p = 0; p <= B; ++p) iota[p] = p;
+    H.d_iota = dev_alloc<int64_t>(B + 1);
+    QG_CUDA(cudaMemcpyAsync(H.d_iota, iota.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+    QG_CUDA(cudaStreamSynchronize(st));  // iota is a stack vector
+  }
   trace("workspace");
 
   // embedding: z = (x, y - s, 1); Pi z; D Pi prep; P xbar, xbar'P xbar
@@ -323,7 +333,12 @@ static cudaGraph_t capture_graph(Handle &H, const Mats &M, bool jvp, int iters) 
 
 // Launch `iters` LSMR iterations of handle H as one graph on `st`.
 static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
-  const auto key = std::make_pair(jvp ? 1 : 0, iters);
+  if (H.comm && !H.comm->capturable()) {  // host-synchronised exchange: plain launches
+    capture_iters(H, M, jvp, iters, st);
+    return;
+  }
+  // partitioned graphs carry the exchange nodes: a different topology
+  const auto key = std::make_pair((jvp ? 1 : 0) + (H.comm ? 2 : 0), iters);
   std::lock_guard<std::mutex> lock(g_graph_mu);
   auto git = g_graphs.find(&H);
   if (git == g_graphs.end()) git = g_graphs.emplace(&H, new GraphCache()).first;
@@ -355,7 +370,10 @@ static int *pinned_word() {
 }
 
 static int kernels_per_iter(const Handle &H) {
-  // k_step<F>, k_step<F'> (one carries the deferred update), 2 x k_fin
+  // k_step<F>, k_step<F'> (one carries the deferred update), 2 x k_fin;
+  // row-partitioned: each step is X_PARTIAL + X_FINISH and each finalize is
+  // k_part_reduce + k_fin (the NCCL kernels are not ours)
+  if (H.comm) return 8 - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
   return 4 - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
@@ -373,7 +391,7 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
     const long long want = done == 0 ? std::min<long long>(rem, 16) : rem;
     const int g = want >= 64 ? 64 : (want >= 16 ? 16 : (want >= 4 ? 4 : 1));
     launch_iters(H, M, jvp, g, st);
-    count_launch(g * kernels_per_iter(H));
+    if (!H.comm || H.comm->capturable()) count_launch(g * kernels_per_iter(H));  // else counted as launched
     done += g;
   }
 }
@@ -456,10 +474,11 @@ const char *qg_last_error(void) { return g_last_error.c_str(); }
 const char *qg_version(void) { return "qcpgrad 0.1.0 (sm_100a)"; }
 int64_t qg_kernel_launches(void) { return g_launches.load(); }
 
-int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream) {
+static int create_batch(qg_handle **out, const qg_batch_desc *desc, qg_comm *comm, void *stream) {
   QG_API_BEGIN
   cudaStream_t st = (cudaStream_t)stream;
   auto *H = new Handle();
+  H->comm = reinterpret_cast<Comm *>(comm);
   try {
     build_handle(*H, *desc, st);
     launch_sub(H->ybar, H->cones.d_zmid, H->sbar, H->NY, st);
@@ -470,6 +489,15 @@ int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream) {
   }
   *out = reinterpret_cast<qg_handle *>(H);
   QG_API_END
+}
+
+int qg_create_batch(qg_handle **out, const qg_batch_desc *desc, void *stream) {
+  return create_batch(out, desc, nullptr, stream);
+}
+
+int qg_create_batch_dist(qg_handle **out, const qg_batch_desc *desc, qg_comm *comm, void *stream) {
+  if (!comm) return fail(QG_ERR_VALIDATION, "qg_create_batch_dist needs a communicator");
+  return create_batch(out, desc, comm, stream);
 }
 
 int qg_destroy(qg_handle *h) {
@@ -602,6 +630,7 @@ int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds, c
 int qg_check(qg_handle *h, const double *x, const double *y, const double *s, double *report, void *stream) {
   QG_API_BEGIN
   Handle &H = *reinterpret_cast<Handle *>(h);
+  if (H.comm) throw Error{QG_ERR_VALIDATION, "qg_check is not available on a row-partitioned handle"};
   std::lock_guard<std::mutex> lock(H.mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace &W = H.ws;

@@ -27,7 +27,10 @@ __device__ __forceinline__ void write_slots(double (&acc)[kSlots], double *red, 
 }
 
 // rhs = -D_theta Q(u)[dtheta] / |z_N|, u = (xbar, ybar, tau).
-__global__ void __launch_bounds__(kThreads) k_jvp_rhs(Mats M, PertDev d, double *u, double *part) {
+// Row-partitioned handles run it twice around the exchange (XMode): X_PARTIAL
+// writes this rank's dA_r' ybar to xred, X_FINISH completes the X rows.
+__global__ void __launch_bounds__(kThreads) k_jvp_rhs(Mats M, PertDev d, double *u, double *part, int xmode,
+                                                      double *xred) {
   __shared__ double red[kWarps * kSlots];
   bool isx;
   const Unit un = unit_of(M, isx);
@@ -38,11 +41,16 @@ __global__ void __launch_bounds__(kThreads) k_jvp_rhs(Mats M, PertDev d, double 
   for (int base = un.row0 + warp * gpw; base < un.row1; base += kWarps * gpw) {
     const int r = base + lane / G;
     const bool valid = r < un.row1;
-    if (isx) {
-      double s1 = valid ? row_dot(d.dP_rp, d.dP_col, d.dP_val, M.xbar, r, lg, G) : 0.0;
+    if (isx && xmode == X_PARTIAL) {
       double s2 = valid ? row_dot(d.dAT_rp, d.dAT_col, d.dAT_val, M.ybar, r, lg, G) : 0.0;
+      s2 = gsum(s2, G);
+      if (valid && lg == 0) xred[r] = s2;
+    } else if (isx) {
+      double s1 = valid ? row_dot(d.dP_rp, d.dP_col, d.dP_val, M.xbar, r, lg, G) : 0.0;
+      double s2 = (valid && xmode == X_FULL) ? row_dot(d.dAT_rp, d.dAT_col, d.dAT_val, M.ybar, r, lg, G) : 0.0;
       s1 = gsum(s1, G);
       s2 = gsum(s2, G);
+      if (valid && xmode == X_FINISH) s2 = xred[r];
       if (valid && lg == 0) {
         const double out = (s1 + s2) + E.tau * d.dq[r];
         const double rhs = (-out) / fabs(E.zN);
@@ -63,6 +71,10 @@ __global__ void __launch_bounds__(kThreads) k_jvp_rhs(Mats M, PertDev d, double 
       }
     }
   }
+  if (isx && xmode == X_PARTIAL) return;  // CTA-uniform: X slots come from X_FINISH
+  if (isx && !M.x_owner)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;
   write_slots(acc, red, part);
 }
 
@@ -87,6 +99,9 @@ __global__ void __launch_bounds__(kThreads) k_vjp_rhs(Mats M, const double *dx, 
       acc[2] += v * v;
     }
   }
+  if (isx && !M.x_owner)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;
   write_slots(acc, red, part);
 }
 
@@ -271,9 +286,21 @@ inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t);
 static unsigned units_grid(const Handle &H) { return (unsigned)(H.nxu() + H.nyu()); }
 
 void launch_jvp_rhs(const Handle &H, const Mats &M, const PertDev &d, double *u, double *part, cudaStream_t st) {
-  if (!units_grid(H)) return;
-  k_jvp_rhs<<<units_grid(H), kThreads, 0, st>>>(M, d, u, part);
-  QG_LAUNCHED();
+  if (!H.comm) {
+    if (!units_grid(H)) return;
+    k_jvp_rhs<<<units_grid(H), kThreads, 0, st>>>(M, d, u, part, X_FULL, nullptr);
+    QG_LAUNCHED();
+    return;
+  }
+  if (units_grid(H)) {
+    k_jvp_rhs<<<units_grid(H), kThreads, 0, st>>>(M, d, u, part, X_PARTIAL, H.xred);
+    QG_LAUNCHED();
+  }
+  H.comm->allreduce(H.xred, H.NX, st);  // every rank, even with no rows of its own
+  if (H.nxu()) {
+    k_jvp_rhs<<<H.nxu(), kThreads, 0, st>>>(M, d, u, part, X_FINISH, H.xred);
+    QG_LAUNCHED();
+  }
 }
 
 void launch_vjp_rhs(const Handle &H, const Mats &M, const double *dx, const double *dy, const double *ds,

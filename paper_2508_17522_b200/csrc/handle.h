@@ -8,6 +8,7 @@
 #include <mutex>
 #include <vector>
 
+#include "comm.h"
 #include "cone_table.h"
 #include "qg_common.cuh"
 
@@ -95,6 +96,13 @@ struct Handle {
   Embed *emb = nullptr;
   Workspace ws;
   std::mutex mu;  // one jvp/vjp at a time per handle (workspace reuse)
+
+  // row-partitioned mode (comm.h): this handle holds one rank's Y rows
+  Comm *comm = nullptr;           // not owned; null = whole problems
+  double *xred = nullptr;         // [NX] A_r' partial products, summed over ranks
+  double *psum = nullptr;         // [2][B][kSlots] per-problem X / Y partial sums
+  int64_t *d_iota = nullptr;      // [B+1] 0..B (one reduced "unit" per problem)
+  bool x_owner() const { return comm == nullptr || comm->rank == 0; }
 
   int nxu() const { return (int)xunits.size(); }
   int nyu() const { return (int)cones.units.size(); }

@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
   // deferred vector update of the previous iteration over the unit's own rows
   // (in = v_k on the u-step): lsmr.py:142-144, ||x||^2 partial in slot 3
   const Lsmr *L = a.st ? a.st + p : nullptr;
-  if (a.upd_h && L && L->itn > 0) {
+  if (a.upd_h && L && L->itn > 0 && !(isx && a.xmode == X_PARTIAL)) {
     const double c1 = L->c_hbar, c2 = L->c_x, c3 = L->c_h, sv = L->s_v;
     const int64_t off = isx ? 0 : M.NX;
     for (int64_t r = off + u.row0 + threadIdx.x; r < off + u.row1; r += blockDim.x) {
@@ -152,9 +152,13 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
 
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
-    for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, M.gx,
-             M.xoff[p], M.yoff[p],
-             [&](int r, double s1, double s2) {
+    if (a.xmode == X_PARTIAL) {
+      // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
+      for_rows(u, M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
+               M.gx, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
+      return;  // CTA-uniform; the X slots are written by the X_FINISH launch
+    }
+    auto xrow = [&](int r, double s1, double s2) {
                const double w = inX[r];
                double res;
                if (KIND == STEP_F) {
@@ -171,7 +175,16 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
                const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
                a.out[r] = o;
                acc[2] += o * o;
-             });
+             };
+    if (a.xmode == X_FINISH)
+      for_rows(u, M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, M.gx,
+               M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
+    else
+      for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, M.gx,
+               M.xoff[p], M.yoff[p], xrow);
+    if (!M.x_owner)
+#pragma unroll
+      for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;  // replicated rows: rank 0 counts them
   } else {
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
@@ -265,6 +278,7 @@ __global__ void __launch_bounds__(kThreads) k_update(Mats M, UpdArgs a) {
     a.x[r] = x;
     acc[0] += x * x;
   }
+  if (isx && !M.x_owner) acc[0] = 0.0;
   double tot[kSlots];
   cta_sum_slots(acc, red, tot);
   if (threadIdx.x == 0)
@@ -326,6 +340,30 @@ __device__ __forceinline__ bool stop_test(Lsmr *L, double xx, double xN) {
   if (stop) { L->active = 0; L->converged = 1; return true; }
   if (L->itn >= L->max_iter) { L->active = 0; L->converged = 0; return true; }
   return false;
+}
+
+// Per-problem sums of the unit partials in exactly k_fin's order (row-
+// partitioned mode): psum = [X sums: B x kSlots | Y sums: B x kSlots].
+__global__ void k_part_reduce(const double *px, const int64_t *px_ptr, const double *py, const int64_t *py_ptr,
+                              int B, double *psum) {
+  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= B) return;
+  double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
+  for (int64_t k = px_ptr[p] + lane; k < px_ptr[p + 1]; k += 32)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) sx[j] += px[k * kSlots + j];
+  for (int64_t k = py_ptr[p] + lane; k < py_ptr[p + 1]; k += 32)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) sy[j] += py[k * kSlots + j];
+#pragma unroll
+  for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) {
+      psum[(size_t)p * kSlots + j] = sx[j];
+      psum[((size_t)B + p) * kSlots + j] = sy[j];
+    }
 }
 
 __global__ void k_fin(Mats M, FinArgs a) {
@@ -553,13 +591,32 @@ Mats make_mats(const Handle &H) {
   M.xt_ptr = H.d_xt_ptr; M.yt_ptr = H.d_yt_ptr;
   M.part_t = H.ws.part_t;
   M.part_u = H.ws.part;
+  M.x_owner = H.x_owner() ? 1 : 0;
   return M;
 }
 
 static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
 
-void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
-  const unsigned grid = (unsigned)(H.nxu() + H.nyu());
+static void launch_step_one(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
+
+// One operator step.  Row-partitioned handles split it around the exchange:
+// X_PARTIAL (Y rows + this rank's A' partials) -> sum over ranks -> X_FINISH.
+void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a0, cudaStream_t st) {
+  if (!H.comm) {
+    launch_step_one(H, M, kind, a0, st);
+    return;
+  }
+  StepArgs a = a0;
+  a.xred = H.xred;
+  a.xmode = X_PARTIAL;
+  launch_step_one(H, M, kind, a, st);
+  H.comm->allreduce(H.xred, H.NX, st);
+  a.xmode = X_FINISH;
+  launch_step_one(H, M, kind, a, st);
+}
+
+static void launch_step_one(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
+  const unsigned grid = (unsigned)(a.xmode == X_FINISH ? H.nxu() : H.nxu() + H.nyu());
   if (grid == 0) return;
   const size_t smem = step_smem(H);
   static int threads = 0;
@@ -567,11 +624,14 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
     const char *e = std::getenv("QG_STEP_THREADS");
     threads = e ? std::max(32, std::min(kStepThreads, std::atoi(e))) : kStepThreads;
   }
-  // Occupancy target: SELL loops keep many loads in flight per thread (64
-  // registers, 8 CTAs/SM measured best); the CSR group path gains from 12
-  // CTAs/SM (c3: 11.2 -> 8.7 ms per jvp).  QG_STEP_MINB=8|12 overrides.
+  // Occupancy target: the SELL F step keeps many loads in flight per thread
+  // (64 registers, 8 CTAs/SM measured best: c5a 0.460 vs 0.509 ms); the F'
+  // step (two-pass Y side, epilogue) and the CSR group path gain from 12
+  // CTAs/SM (c5a F' 0.625 -> 0.574 ms; c3: 11.2 -> 8.7 ms per jvp).
+  // QG_STEP_MINB=8|12 overrides.
   static const char *env_minb = std::getenv("QG_STEP_MINB");
-  const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (H.nslice_x + H.nslice_y > 0 ? 8 : 12);
+  const bool sell = H.nslice_x + H.nslice_y > 0;
+  const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (sell && kind == STEP_F ? 8 : 12);
   auto go = [&](auto kern, size_t sm_bytes) {
     if (sm_bytes > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
@@ -592,6 +652,16 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
   a.py = H.ws.part + (size_t)H.nxu() * kSlots;
   a.py_ptr = H.d_yunit_ptr;
   const unsigned grid = (unsigned)((H.B * 32 + 255) / 256);
+  if (H.comm) {
+    // row-partitioned: per-problem sums (k_fin's order), summed over ranks,
+    // then k_fin reads one reduced unit per problem
+    k_part_reduce<<<grid, 256, 0, st>>>(a.px, a.px_ptr, a.py, a.py_ptr, H.B, H.psum);
+    QG_LAUNCHED();
+    H.comm->allreduce(H.psum, 2 * (int64_t)H.B * kSlots, st);
+    a.px = H.psum;
+    a.py = H.psum + (size_t)H.B * kSlots;
+    a.px_ptr = a.py_ptr = H.d_iota;
+  }
   k_fin<<<grid, 256, 0, st>>>(M, a);
   QG_LAUNCHED();
 }

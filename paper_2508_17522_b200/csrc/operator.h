@@ -25,6 +25,8 @@ struct StepArgs {
   // hbar = h - c1 hbar ; x += c2 hbar ; h = in s_v - c3 h over the unit's own
   // rows, ||x||^2 partial in slot 3 (lsmr.py:142-144, 168)
   double *upd_h = nullptr, *upd_hb = nullptr, *upd_x = nullptr;
+  int xmode = X_FULL;         // row-partitioned mode phase (ops_dev.cuh)
+  double *xred = nullptr;     // [NX] A' partials (X_PARTIAL writes, X_FINISH reads)
 };
 
 struct FinArgs {

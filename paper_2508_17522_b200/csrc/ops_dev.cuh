@@ -26,7 +26,15 @@ struct Mats {
   const int64_t *xt_ptr, *yt_ptr;       // [B+1] task ranges per problem
   double *part_t;                       // per-task partial sums
   double *part_u;                       // per-unit partial sums (X units then Y units)
+  int x_owner;                          // 0: X rows are replicated and counted by rank 0 only
 };
+
+// Row-partitioned mode, X side of an operator step / rhs assembly:
+//   X_FULL    normal fused X rows (whole problems)
+//   X_PARTIAL X units write this rank's A' partial product to xred (no row
+//             update); Y units run as usual
+//   X_FINISH  X units only: row update with the summed A' product from xred
+enum XMode : int { X_FULL = 0, X_PARTIAL = 1, X_FINISH = 2 };
 
 // Two slices of one matrix at once (independent load streams -> twice the
 // memory-level parallelism per warp); slice b may be absent (sb < 0).  Each

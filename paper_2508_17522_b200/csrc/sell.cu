@@ -259,9 +259,11 @@ void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<in
   };
   const bool sx = sell_ok(H.NX, (int64_t)rpP[H.NX] + rpAT[H.NX]);
   const bool sy = sell_ok(H.NY, (int64_t)rpA[H.NY]);
-  // 16-bit problem-local column indices when every problem is small enough
+  // 16-bit problem-local column indices (every problem small enough): opt-in
+  // with QG_SELL16=1 -- measured slower than 32-bit on c5a (the gathers are
+  // latency-, not byte-bound; the local base costs an extra add per entry)
   const char *f16 = std::getenv("QG_SELL16");
-  bool small = f16 ? std::atoi(f16) != 0 : true;
+  bool small = f16 ? std::atoi(f16) != 0 : false;
   for (int p = 0; p < H.B && small; ++p) small = H.n[p] < 65536 && H.m[p] < 65536;
   const auto *bx = small ? &H.xoff : nullptr, *by = small ? &H.yoff : nullptr;
   H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,

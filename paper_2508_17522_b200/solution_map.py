@@ -171,23 +171,25 @@ class QCPBatch:
         self._sol_dev = (dev["x"], dev["y"], dev["s"])
 
     @classmethod
-    def from_device(cls, n, m, P_nnz, A_nnz, blocks, tensors):
-        """Create from concatenated CUDA tensors (keys as in ``qg_batch_desc``)."""
+    def from_device(cls, n, m, P_nnz, A_nnz, blocks, tensors, comm=None):
+        """Create from concatenated CUDA tensors (keys as in ``qg_batch_desc``).
+        With ``comm`` (``dist.Comm``) the tensors are this rank's row shard of
+        a row-partitioned batch (``dist.py``)."""
         self = cls.__new__(cls)
         self.thetas = self.sols = None
-        self._create(n, m, P_nnz, A_nnz, blocks, tensors)
+        self._create(n, m, P_nnz, A_nnz, blocks, tensors, comm)
         self._sol_dev = (tensors["x"], tensors["y"], tensors["s"])
         return self
 
     @classmethod
-    def from_host(cls, n, m, P_nnz, A_nnz, blocks, arrays):
+    def from_host(cls, n, m, P_nnz, A_nnz, blocks, arrays, comm=None):
         """Create from concatenated HOST arrays (NumPy or pinned torch CPU
         tensors, keys as in ``qg_batch_desc``): the host-buffer boundary."""
         import torch
 
         f64, i64 = torch.float64, torch.int64
         t = {k: N.to_dev(v, i64 if k.endswith(("colptr", "rowidx")) else f64) for k, v in arrays.items()}
-        return cls.from_device(n, m, P_nnz, A_nnz, blocks, t)
+        return cls.from_device(n, m, P_nnz, A_nnz, blocks, t, comm=comm)
 
     def jvp_host(self, dP, dA, dq, db, **kw):
         """jvp from concatenated host arrays on the patterns of P / A; returns
@@ -219,7 +221,7 @@ class QCPBatch:
         N.check(N.lib().qg_time_kernel(self._h, int(which), int(reps), N.ctypes.byref(ms), N.stream_ptr()))
         return float(ms.value)
 
-    def _create(self, n, m, P_nnz, A_nnz, blocks, t):
+    def _create(self, n, m, P_nnz, A_nnz, blocks, t, comm=None):
         lib = N.lib()
         self.B = len(n)
         self.n, self.m = [int(v) for v in n], [int(v) for v in m]
@@ -242,8 +244,11 @@ class QCPBatch:
         for k in ("P_colptr", "P_rowidx", "P_vals", "A_colptr", "A_rowidx", "A_vals", "q", "b", "x", "y", "s"):
             setattr(d, k, t[k].data_ptr())
         h = N.c_vp()
-        N.check(lib.qg_create_batch(N.ctypes.byref(h), N.ctypes.byref(d), N.stream_ptr()))
-        self._h, self._lib = h, lib
+        if comm is None:
+            N.check(lib.qg_create_batch(N.ctypes.byref(h), N.ctypes.byref(d), N.stream_ptr()))
+        else:
+            N.check(lib.qg_create_batch_dist(N.ctypes.byref(h), N.ctypes.byref(d), comm.ptr, N.stream_ptr()))
+        self._h, self._lib, self._comm = h, lib, comm  # the handle keeps the communicator alive
 
     def close(self):
         if getattr(self, "_h", None):
