@@ -155,6 +155,21 @@ int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stre
 /* Number of kernels this library launched since load (telemetry). */
 int64_t qg_kernel_launches(void);
 
+/* ---- re-solving oracle (testkit.refine / fd_jvp, testkit.py:410-497) ----
+ * Move the handle to an arbitrary embedding point z = [X | Y | T] (device,
+ * NE = sum n + sum m + nprob doubles, every z_N > 0 else QG_ERR_DOMAIN):
+ * Pi z, P xbar, and with want_deriv the projection derivative at z.  jvp /
+ * vjp need z_N = 1 (QG_ERR_DOMAIN otherwise, solution_map.py:197-203). */
+int qg_set_point(qg_handle *h, const double *z, int want_deriv, void *stream);
+/* normalized residual N(z) = (Q(Pi z) - Pi z + z)/|z_N| at the handle's point
+ * (embedding.normalized_residual, embedding.py:374-396); out: NE doubles */
+int qg_residual(qg_handle *h, double *out, void *stream);
+/* LSMR on J = F - rank1 e_N' (rank1: NE doubles, or NULL for F itself) at the
+ * handle's point from rhs (NE), solution to sol (NE); the Gauss-Newton model
+ * of testkit.refine (testkit.py:439-454).  diag[nprob] (host). */
+int qg_lsmr_jacobian(qg_handle *h, const double *rhs, const double *rank1, const qg_lsmr_opts *opts,
+                     double *sol, qg_diag *diag, void *stream);
+
 /* ---- row-partitioned mode (no reference counterpart:
  * the reference is single-process).  The Y rows of A -- with b, y, s and
  * whole cone blocks (zero / nonneg blocks may be cut anywhere) -- are split

@@ -52,7 +52,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(part_t);
+  dev_free(st); dev_free(d_nactive); dev_free(part_t); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -92,14 +92,6 @@ Handle::~Handle() {
   }
   for (auto &kv : g_exec)
     if (kv.second.owner == this) kv.second.owner = nullptr;  // must be re-pointed before next use
-}
-
-static int pick_group(int64_t nnz, int64_t rows) {
-  if (rows <= 0) return 1;
-  const double avg = (double)nnz / (double)rows;
-  int g = 1;
-  while (g < 32 && g < avg * 0.75) g <<= 1;
-  return g;
 }
 
 // ------------------------------------------------------------ create ----
@@ -160,8 +152,6 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   QG_CUDA(cudaStreamSynchronize(st));
   trace("rowptr D2H");
   const int64_t nnzX = (int64_t)rpP[H.NX] + rpAT[H.NX], nnzY = rpA[H.NY];
-  H.gx = pick_group(nnzX, H.NX);
-  H.gy = pick_group(nnzY, H.NY);
   // aim for >= 4 CTAs per SM when the batch is large enough, 2k..16k entries per unit
   const int64_t total = nnzX + nnzY + H.NX + H.NY;
   // small problems get small units (all SMs busy, short per-warp chains),
@@ -286,17 +276,22 @@ static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStr
   // kernel of iteration k+1 (which streams v_k anyway), and its stopping
   // test runs at the head of that iteration's PH_STEP_U finalize; the last
   // iteration's update is flushed by lsmr_flush().  4 launches / iteration.
+  const double *rk1 = H.use_rk1 ? W.rk1 : nullptr;
   for (int i = 0; i < iters; ++i) {
     StepArgs su{W.v, W.dpv, W.u, W.u, ku == STEP_FT ? W.dpu : nullptr, W.tY, W.tY2, W.st, 0, W.part};
     su.upd_h = W.h;
     su.upd_hb = W.hb;
     su.upd_x = W.x;
+    su.rk1 = rk1;
     launch_step(H, M, ku, su, st);
     FinArgs fu{H.B, PH_STEP_U, ku, W.st, W.part, W.v, W.u, W.u, W.h, W.hb, W.x, W.v};
+    fu.rk1 = rk1;
     launch_fin(H, M, fu, st);
     StepArgs sv{W.u, W.dpu, W.v, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 1, W.part};
+    sv.rk1 = rk1;
     launch_step(H, M, kv, sv, st);
     FinArgs fv{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
+    fv.rk1 = rk1;
     launch_fin(H, M, fv, st);
   }
 }
@@ -338,7 +333,7 @@ static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStre
     return;
   }
   // partitioned graphs carry the exchange nodes: a different topology
-  const auto key = std::make_pair((jvp ? 1 : 0) + (H.comm ? 2 : 0), iters);
+  const auto key = std::make_pair((jvp ? 1 : 0) + (H.comm ? 2 : 0) + (H.use_rk1 ? 4 : 0), iters);
   std::lock_guard<std::mutex> lock(g_graph_mu);
   auto git = g_graphs.find(&H);
   if (git == g_graphs.end()) git = g_graphs.emplace(&H, new GraphCache()).first;
@@ -445,8 +440,10 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
   launch_fin(H, M, fr, st);
   const int kv = jvp ? STEP_FT : STEP_F;
   StepArgs s0{W.u, W.dpu, nullptr, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 0, W.part};
+  s0.rk1 = H.use_rk1 ? W.rk1 : nullptr;
   launch_step(H, M, kv, s0, st);
   FinArgs f0{H.B, PH_INIT_V, kv, W.st, W.part, W.u, nullptr, W.v, W.h, W.hb, W.x, W.v};
+  f0.rk1 = s0.rk1;
   launch_fin(H, M, f0, st);
   UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
   launch_update(H, M, ua, st);
@@ -543,6 +540,7 @@ int qg_apply_F(qg_handle *h, int transpose, const double *w, double *out, void *
   QG_API_BEGIN
   Handle &H = *reinterpret_cast<Handle *>(h);
   std::lock_guard<std::mutex> lock(H.mu);
+  if (!H.deriv_ready) throw Error{QG_ERR_VALIDATION, "projection derivative not prepared at the current point"};
   cudaStream_t st = (cudaStream_t)stream;
   Workspace &W = H.ws;
   Mats M = make_mats(H);
@@ -556,11 +554,49 @@ int qg_apply_F(qg_handle *h, int transpose, const double *w, double *out, void *
   QG_API_END
 }
 
+// jvp / vjp formulas hold at a normalized embedding (solution_map.py:197-203)
+static void require_normalized(const Handle &H) {
+  if (!H.normalized)
+    throw Error{QG_ERR_DOMAIN, "derivative formulas require the normalized embedding z_N = 1"};
+  if (!H.deriv_ready) throw Error{QG_ERR_VALIDATION, "projection derivative not prepared at the current point"};
+}
+
+// Move the handle to the embedding point z = [X | Y | T] (refine, testkit.py
+// :410-470): x part, middle block, z_N per problem; Pi z, P xbar, x'Px and
+// (want_deriv) D Pi at the new point.  z_N <= 0 is a DomainError
+// (embedding.py:384-387, 413-414).
+static void set_point(Handle &H, const double *z, bool want_deriv, cudaStream_t st) {
+  std::vector<double> zt(H.B);
+  QG_CUDA(cudaMemcpyAsync(zt.data(), z + H.NX + H.NY, sizeof(double) * H.B, cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  bool norm = true;
+  for (int p = 0; p < H.B; ++p) {
+    if (!(zt[p] > 0.0))
+      throw Error{QG_ERR_DOMAIN, (H.B > 1 ? "problem " + std::to_string(p) + ": " : std::string()) +
+                                     "the point needs z_N > 0, got z_N = " + std::to_string(zt[p])};
+    norm = norm && zt[p] == 1.0;
+  }
+  H.normalized = false;  // until the new point is fully in place
+  H.deriv_ready = false;
+  if (H.NX) QG_CUDA(cudaMemcpyAsync(H.xbar, z, sizeof(double) * H.NX, cudaMemcpyDeviceToDevice, st));
+  double *zmid = H.cones.d_zmid;
+  if (H.NY) QG_CUDA(cudaMemcpyAsync(zmid, z + H.NX, sizeof(double) * H.NY, cudaMemcpyDeviceToDevice, st));
+  H.cones.prepare(zmid, H.ybar, 1, want_deriv, st);
+  H.cones.check_errors(st);
+  Mats M = make_mats(H);
+  launch_embed_consts(H, M, H.ws.part, st, z + H.NX + H.NY);
+  launch_sub(H.ybar, zmid, H.sbar, H.NY, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  H.normalized = norm;
+  H.deriv_ready = want_deriv;
+}
+
 int qg_jvp(qg_handle *h, const qg_perturbation *d, const qg_lsmr_opts *opts, double *dx, double *dy, double *ds,
            qg_diag *diag, void *stream) {
   QG_API_BEGIN
   Handle &H = *reinterpret_cast<Handle *>(h);
   std::lock_guard<std::mutex> lock(H.mu);
+  require_normalized(H);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace &W = H.ws;
   Mats M = make_mats(H);
@@ -610,6 +646,7 @@ int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds, c
   QG_API_BEGIN
   Handle &H = *reinterpret_cast<Handle *>(h);
   std::lock_guard<std::mutex> lock(H.mu);
+  require_normalized(H);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace &W = H.ws;
   Mats M = make_mats(H);
@@ -623,6 +660,59 @@ int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds, c
   lsmr_solve(H, M, false, RHS_VJP, cap, st);
   lsmr_finish(H, diag, st);
   launch_vjp_grad(H, M, W.x, dP_vals, dA_vals, dq, db, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+int qg_set_point(qg_handle *h, const double *z, int want_deriv, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  if (H.comm) throw Error{QG_ERR_VALIDATION, "qg_set_point is not available on a row-partitioned handle"};
+  set_point(H, z, want_deriv != 0, (cudaStream_t)stream);
+  QG_API_END
+}
+
+int qg_residual(qg_handle *h, double *out, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  if (H.comm) throw Error{QG_ERR_VALIDATION, "qg_residual is not available on a row-partitioned handle"};
+  cudaStream_t st = (cudaStream_t)stream;
+  Mats M = make_mats(H);
+  launch_residual(H, M, out, H.ws.part, st);
+  QG_CUDA(cudaStreamSynchronize(st));
+  QG_API_END
+}
+
+// LSMR on J = F - r e_N' (r = rank1, or F alone when rank1 is null) from the
+// right-hand side rhs; the solution (embedding layout) goes to sol.
+// testkit.refine's Gauss-Newton model (testkit.py:439-454).
+int qg_lsmr_jacobian(qg_handle *h, const double *rhs, const double *rank1, const qg_lsmr_opts *opts, double *sol,
+                     qg_diag *diag, void *stream) {
+  QG_API_BEGIN
+  Handle &H = *reinterpret_cast<Handle *>(h);
+  std::lock_guard<std::mutex> lock(H.mu);
+  if (!H.deriv_ready) throw Error{QG_ERR_VALIDATION, "projection derivative not prepared at the current point"};
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace &W = H.ws;
+  Mats M = make_mats(H);
+  if (rank1) {
+    if (!W.rk1) W.rk1 = dev_alloc<double>(H.NE);
+    QG_CUDA(cudaMemcpyAsync(W.rk1, rank1, sizeof(double) * H.NE, cudaMemcpyDeviceToDevice, st));
+  }
+  struct Rk1Scope {
+    Handle &H;
+    Rk1Scope(Handle &h, bool on) : H(h) { H.use_rk1 = on; }
+    ~Rk1Scope() { H.use_rk1 = false; }
+  } scope(H, rank1 != nullptr);
+  long long cap;
+  lsmr_begin(H, *opts, st, cap);
+  QG_CUDA(cudaMemcpyAsync(W.u, rhs, sizeof(double) * H.NE, cudaMemcpyDeviceToDevice, st));
+  launch_vec_rhs(H, M, W.u, W.u, W.part, st);
+  lsmr_solve(H, M, true, RHS_VEC, cap, st);
+  lsmr_finish(H, diag, st);
+  QG_CUDA(cudaMemcpyAsync(sol, W.x, sizeof(double) * H.NE, cudaMemcpyDeviceToDevice, st));
   QG_CUDA(cudaStreamSynchronize(st));
   QG_API_END
 }

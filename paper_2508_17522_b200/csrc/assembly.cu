@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kThreads) k_jvp_rhs(Mats M, PertDev d, double 
   const Unit un = unit_of(M, isx);
   const Embed E = M.emb[un.prob];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = isx ? M.gx : M.gy, lg = lane & (G - 1), gpw = 32 / G;
+  const int G = un.lanes, lg = lane & (G - 1), gpw = 32 / G;
   double acc[kSlots] = {0, 0, 0, 0};
   for (int base = un.row0 + warp * gpw; base < un.row1; base += kWarps * gpw) {
     const int r = base + lane / G;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kThreads) k_pxbar(Mats M, double *Pxbar, doubl
   __shared__ double red[kWarps * kSlots];
   const Unit un = M.xu[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = M.gx, lg = lane & (G - 1), gpw = 32 / G;
+  const int G = un.lanes, lg = lane & (G - 1), gpw = 32 / G;
   double acc[kSlots] = {0, 0, 0, 0};
   for (int base = un.row0 + warp * gpw; base < un.row1; base += kWarps * gpw) {
     const int r = base + lane / G;
@@ -194,7 +194,8 @@ __global__ void __launch_bounds__(kThreads) k_pxbar(Mats M, double *Pxbar, doubl
   write_slots(acc, red, part);
 }
 
-__global__ void k_embed_fin(Mats M, const double *part, Embed *emb, int B) {
+// zT: the points' T coordinates (B values), or null for embed()'s z_N = 1.
+__global__ void k_embed_fin(Mats M, const double *part, Embed *emb, int B, const double *zT) {
   const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (p >= B) return;
@@ -203,7 +204,7 @@ __global__ void k_embed_fin(Mats M, const double *part, Embed *emb, int B) {
   s = warp_sum(s);
   if (lane == 0) {
     Embed E;
-    E.zN = 1.0;                       // embed(): last coordinate exactly 1
+    E.zN = zT ? zT[p] : 1.0;          // embed(): last coordinate exactly 1
     E.tau = fmax(E.zN, 0.0);
     E.last = E.zN > 0.0 ? 1.0 : 0.0;
     E.xPx = s;
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(kThreads) k_kkt(Mats M, const double *x, const
   bool isx;
   const Unit un = unit_of(M, isx);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int G = isx ? M.gx : M.gy, lg = lane & (G - 1), gpw = 32 / G;
+  const int G = un.lanes, lg = lane & (G - 1), gpw = 32 / G;
   double acc[kSlots] = {0, 0, 0, 0};
   for (int base = un.row0 + warp * gpw; base < un.row1; base += kWarps * gpw) {
     const int r = base + lane / G;
@@ -277,6 +278,75 @@ __global__ void k_csr_spmv(const int32_t *rp, const int32_t *col, const double *
   for (int k = rp[r] + lane; k < rp[r + 1]; k += 32) s += val[k] * x[col[k]];
   s = warp_sum(s);
   if (lane == 0) out[r] = s;
+}
+
+// Normalized residual N(z) = (Q(Pi z) - Pi z + z) / |z_N| at the handle's
+// point (embedding.py:198-211, 374-396): X / Y rows here, T in k_residual_fin.
+// Partials: X [.., q'x], Y [b'y].
+__global__ void __launch_bounds__(kThreads) k_residual(Mats M, double *out, double *part) {
+  __shared__ double red[kWarps * kSlots];
+  bool isx;
+  const Unit un = unit_of(M, isx);
+  const Embed E = M.emb[un.prob];
+  const double inv = 1.0 / fabs(E.zN);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int G = un.lanes, lg = lane & (G - 1), gpw = 32 / G;
+  double acc[kSlots] = {0, 0, 0, 0};
+  for (int base = un.row0 + warp * gpw; base < un.row1; base += kWarps * gpw) {
+    const int r = base + lane / G;
+    const bool valid = r < un.row1;
+    if (isx) {
+      double s = valid ? row_dot(M.AT_rp, M.AT_col, M.AT_val, M.ybar, r, lg, G) : 0.0;
+      s = gsum(s, G);
+      if (valid && lg == 0) {
+        const double x = M.xbar[r];
+        const double qx = (M.Pxbar[r] + s) + E.tau * M.q[r];
+        out[r] = ((qx - x) + x) * inv;
+        acc[1] += M.q[r] * x;
+      }
+    } else {
+      double s = valid ? row_dot(M.A_rp, M.A_col, M.A_val, M.xbar, r, lg, G) : 0.0;
+      s = gsum(s, G);
+      if (valid && lg == 0) {
+        const double qy = (-s) + E.tau * M.b[r];
+        out[M.NX + r] = ((qy - M.ybar[r]) + M.dpi.zmid[r]) * inv;
+        acc[0] += M.b[r] * M.ybar[r];
+      }
+    }
+  }
+  write_slots(acc, red, part);
+}
+
+__global__ void k_residual_fin(Mats M, const double *part, double *out, int B) {
+  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (p >= B) return;
+  double qx = 0.0, by = 0.0;
+  for (int64_t k = M.xu_ptr[p] + lane; k < M.xu_ptr[p + 1]; k += 32) qx += part[k * kSlots + 1];
+  for (int64_t k = M.yu_ptr[p] + lane; k < M.yu_ptr[p + 1]; k += 32) by += part[(M.nxu + k) * kSlots];
+  qx = warp_sum(qx);
+  by = warp_sum(by);
+  if (lane == 0) {
+    const Embed E = M.emb[p];
+    const double qn = ((-E.xPx) / E.tau - qx) - by;
+    out[M.NX + M.NY + p] = ((qn - E.tau) + E.zN) / fabs(E.zN);
+  }
+}
+
+// LSMR right-hand side from a given vector (X / Y rows; T is set by the
+// PH_RHS finalize): u = r, ||u_XY||^2 partials in slot 2.
+__global__ void __launch_bounds__(kThreads) k_vec_rhs(Mats M, const double *r, double *u, double *part) {
+  __shared__ double red[kWarps * kSlots];
+  bool isx;
+  const Unit un = unit_of(M, isx);
+  const int64_t off = isx ? 0 : M.NX;
+  double acc[kSlots] = {0, 0, 0, 0};
+  for (int64_t i = off + un.row0 + threadIdx.x; i < off + un.row1; i += blockDim.x) {
+    const double v = r[i];
+    u[i] = v;
+    acc[2] += v * v;
+  }
+  write_slots(acc, red, part);
 }
 
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
@@ -343,12 +413,27 @@ void launch_embed_prep(const Handle &H, const double *, const double *y, const d
   QG_LAUNCHED();
 }
 
-void launch_embed_consts(const Handle &H, const Mats &M, double *part, cudaStream_t st) {
+void launch_embed_consts(const Handle &H, const Mats &M, double *part, cudaStream_t st, const double *zT) {
   if (H.nxu() > 0) {
     k_pxbar<<<H.nxu(), kThreads, 0, st>>>(M, H.Pxbar, part);
     QG_LAUNCHED();
   }
-  k_embed_fin<<<nb((int64_t)H.B * 32), 256, 0, st>>>(M, part, H.emb, H.B);
+  k_embed_fin<<<nb((int64_t)H.B * 32), 256, 0, st>>>(M, part, H.emb, H.B, zT);
+  QG_LAUNCHED();
+}
+
+void launch_residual(const Handle &H, const Mats &M, double *out, double *part, cudaStream_t st) {
+  if (units_grid(H)) {
+    k_residual<<<units_grid(H), kThreads, 0, st>>>(M, out, part);
+    QG_LAUNCHED();
+  }
+  k_residual_fin<<<nb((int64_t)H.B * 32), 256, 0, st>>>(M, part, out, H.B);
+  QG_LAUNCHED();
+}
+
+void launch_vec_rhs(const Handle &H, const Mats &M, const double *r, double *u, double *part, cudaStream_t st) {
+  if (!units_grid(H)) return;
+  k_vec_rhs<<<units_grid(H), kThreads, 0, st>>>(M, r, u, part);
   QG_LAUNCHED();
 }
 

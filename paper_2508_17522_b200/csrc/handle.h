@@ -61,6 +61,7 @@ struct Workspace {
   double *dpu = nullptr, *dpv = nullptr, *tY = nullptr, *tY2 = nullptr;          // Y
   double *part = nullptr;    // per work-unit partial sums (X units then Y units)
   double *part_t = nullptr;  // per warp-task partial sums of the SpMV steps
+  double *rk1 = nullptr;     // EVec: refine rank-one vector (allocated on first use)
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
   int *h_nactive = nullptr;  // pinned
@@ -80,6 +81,7 @@ struct Handle {
   int32_t *x_rowof = nullptr;   // [32 * x slices] row of each slice lane (-1 = padding)
   int32_t *y_rowof = nullptr;
   int64_t nslice_x = 0, nslice_y = 0;
+  bool has_wide = false;        // some unit runs CTA-per-row (MODE_WIDE)
   std::vector<Task> tasks;      // X tasks [0, ntx) then Y tasks [ntx, ntx + nty)
   std::vector<int64_t> xt_ptr, yt_ptr;   // [B+1] per-problem task ranges (global task index)
   int64_t ntx = 0, nty = 0;
@@ -88,7 +90,6 @@ struct Handle {
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;
-  int gx = 1, gy = 1;            // SpMV group sizes (X rows / Y rows)
   int64_t *d_xoff = nullptr, *d_yoff = nullptr;
   int64_t *d_xunit_ptr = nullptr, *d_yunit_ptr = nullptr;
   double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;
@@ -103,6 +104,11 @@ struct Handle {
   double *psum = nullptr;         // [2][B][kSlots] per-problem X / Y partial sums
   int64_t *d_iota = nullptr;      // [B+1] 0..B (one reduced "unit" per problem)
   bool x_owner() const { return comm == nullptr || comm->rank == 0; }
+
+  // the point z the handle is prepared at (qg_set_point moves it)
+  bool normalized = true;   // z_N == 1 for every problem (jvp / vjp formulas)
+  bool deriv_ready = true;  // D Pi prepared at the current point
+  bool use_rk1 = false;     // LSMR on J = F - rk1 e_N' (qg_lsmr_jacobian)
 
   int nxu() const { return (int)xunits.size(); }
   int nyu() const { return (int)cones.units.size(); }

@@ -35,7 +35,9 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 // Iterate the rows of a unit: MODE_SELL -> one thread per row over the unit's
 // SELL slices; MODE_LONG -> a group of G lanes per CSR row.  `row(r, s1, s2)`
 // receives the row sums of the one or two matrices (second may be unused).
-template <class RowFn>
+// WIDE: compile the CTA-per-row path (MODE_WIDE units exist); kept out of the
+// common kernels, whose SELL loops lose ~15% to its extra shared state.
+template <bool WIDE, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
@@ -60,6 +62,40 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       if (S2) sell_dot2(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
+    }
+  } else if (WIDE && u.mode == MODE_WIDE) {
+    // the whole CTA per CSR row: 4 independent partial sums per thread keep
+    // the loads in flight, then a fixed-order warp / CTA reduction
+    __shared__ double wred[2 * 32];
+    const int nw = (int)(blockDim.x >> 5);
+    for (int r = u.row0; r < u.row1; ++r) {
+      double s1 = wide_dot(rp1, c1, v1, x1, r), s2 = rp2 ? wide_dot(rp2, c2, v2, x2, r) : 0.0;
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) {
+        wred[warp] = s1;
+        wred[32 + warp] = s2;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t1 = wred[0], t2 = wred[32];
+        for (int w = 1; w < nw; ++w) {
+          t1 += wred[w];
+          t2 += wred[32 + w];
+        }
+        row(r, t1, t2);
+      }
+      __syncthreads();
+    }
+  } else if (G == 32) {
+    // warp per row with a compile-time lane stride: the loop unrolls into
+    // independent loads (a runtime stride measured 7x slower on C5b)
+    for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
+      double s1 = row_dot32(rp1, c1, v1, x1, r, lane);
+      double s2 = rp2 ? row_dot32(rp2, c2, v2, x2, r, lane) : 0.0;
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) row(r, s1, s2);
     }
   } else {
     // G lanes per CSR row (G from the average row length of the matrices),
@@ -119,9 +155,16 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
 // 128-thread CTAs: more slice pairs per warp inside a unit (smaller tail at the
 // closing reduction) at the same register-limited occupancy (8 CTAs/SM).
 constexpr int kStepThreads = 128;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4;
+constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
-template <int KIND, int MINB>
+// FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
+// X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
+// a.rk1 is set).  The common variant (0) carries none of them.
+template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
+  constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
+  const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
   const bool isx = (int)blockIdx.x < M.nxu;
@@ -137,7 +180,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
   // deferred vector update of the previous iteration over the unit's own rows
   // (in = v_k on the u-step): lsmr.py:142-144, ||x||^2 partial in slot 3
   const Lsmr *L = a.st ? a.st + p : nullptr;
-  if (a.upd_h && L && L->itn > 0 && !(isx && a.xmode == X_PARTIAL)) {
+  if (a.upd_h && L && L->itn > 0 && !(kDist && isx && a.xmode == X_PARTIAL)) {
     const double c1 = L->c_hbar, c2 = L->c_x, c3 = L->c_h, sv = L->s_v;
     const int64_t off = isx ? 0 : M.NX;
     for (int64_t r = off + u.row0 + threadIdx.x; r < off + u.row1; r += blockDim.x) {
@@ -152,10 +195,10 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
 
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
-    if (a.xmode == X_PARTIAL) {
+    if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
-      for_rows(u, M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
-               M.gx, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
+      for_rows<kWide>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
+               u.lanes, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
     auto xrow = [&](int r, double s1, double s2) {
@@ -166,35 +209,38 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
                  const double o1 = (s1 + s2) + wN * M.q[r];
                  res = ((o1 - w) + w) / E.zN;
                  acc[0] += M.Pxbar[r] * w;
+                 if (kRk1) res -= a.rk1[r] * wN;
                } else {
                  // g1 = P w1 - A' w2 - (2/tau) w_N P xbar - w_N q ; (D Pi (g - w) + w)/z_N
                  const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
                  res = ((g - w) + w) / E.zN;
+                 if (kRk1) acc[3] += a.rk1[r] * w;
                }
                acc[1] += M.q[r] * w;
                const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
                a.out[r] = o;
                acc[2] += o * o;
              };
-    if (a.xmode == X_FINISH)
-      for_rows(u, M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, M.gx,
+    if (kDist && a.xmode == X_FINISH)
+      for_rows<kWide>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
-      for_rows(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, M.gx,
+      for_rows<kWide>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
                M.xoff[p], M.yoff[p], xrow);
-    if (!M.x_owner)
+    if (kDist && !M.x_owner)
 #pragma unroll
       for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;  // replicated rows: rank 0 counts them
   } else {
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
+      for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
                  const double o2 = (-s) + wN * M.b[r];
-                 const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+                 double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+                 if (kRk1) res -= a.rk1[M.NX + r] * wN;
                  const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
                  outY[r] = o;
                  acc[0] += M.b[r] * a.dpin[r];
@@ -202,9 +248,12 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
                });
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
-      for_rows(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, M.gy,
+      for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
-               [&](int r, double s, double) { a.tY[r] = (s - wN * M.b[r]) - inY[r]; });
+               [&](int r, double s, double) {
+                 a.tY[r] = (s - wN * M.b[r]) - inY[r];
+                 if (kRk1) acc[3] += a.rk1[M.NX + r] * inY[r];
+               });
       __syncthreads();
       // per row: o = s_in (D Pi t + w2)/z_N - c_out old ; D Pi o for the next F step
       auto fin_row = [&](int r, double dpt) {
@@ -388,9 +437,16 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (lane != 0) return;
   const Embed E = M.emb[p];
   const int64_t T = M.NX + M.NY + p;
+  // T component of the step output, with the refine rank-one term
+  // (testkit.py:446-451): F: - r_N w_N ; F': - r'w
+  auto tcomp = [&](double wN) {
+    double t = t_component(a.kind, E, wN, sx, sy);
+    if (a.rk1) t -= (a.kind == STEP_F) ? a.rk1[T] * wN : (sx[3] + sy[3]) + a.rk1[T] * wN;
+    return t;
+  };
 
   if (a.phase == PH_APPLY) {
-    a.out[T] = t_component(a.kind, E, a.in[T], sx, sy);
+    a.out[T] = tcomp(a.in[T]);
     return;
   }
   if (a.phase == PH_RHS) {
@@ -399,6 +455,8 @@ __global__ void k_fin(Mats M, FinArgs a) {
     if (a.kind == RHS_JVP) {
       const double outN = ((-sx[0]) / E.tau - sx[1]) - sy[0];   // embedding.py:291
       rN = (-outN) / fabs(E.zN);
+    } else if (a.kind == RHS_VEC) {
+      rN = a.in[T];                                             // given right-hand side
     } else {
       const double dzN = ((-sx[0]) - sy[0]) - sy[1];             // solution_map.py:259
       rN = -dzN;
@@ -427,7 +485,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
     return;
   }
   if (a.phase == PH_INIT_V) {
-    const double vN = t_component(a.kind, E, a.in[T], sx, sy) * L->s_in;
+    const double vN = tcomp(a.in[T]) * L->s_in;
     a.out[T] = vN;
     const double alpha = sqrt((sx[2] + sy[2]) + vN * vN);
     L->alpha = alpha;
@@ -463,7 +521,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (a.phase == PH_STEP_U) {
     if (L->itn > 0 && stop_test(L, sx[3] + sy[3], a.x[T])) return;  // iteration itn ended the solve
     L->itn += 1;
-    const double uN = L->s_in * t_component(a.kind, E, a.in[T], sx, sy) - L->c_out * a.old[T];
+    const double uN = L->s_in * tcomp(a.in[T]) - L->c_out * a.old[T];
     a.out[T] = uN;
     const double beta = sqrt((sx[2] + sy[2]) + uN * uN);
     L->beta = beta;
@@ -481,7 +539,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (a.phase == PH_STEP_V) {
     double alpha = L->alpha;
     if (!L->skip_v) {
-      const double vN = L->s_in * t_component(a.kind, E, a.in[T], sx, sy) - L->c_out * a.old[T];
+      const double vN = L->s_in * tcomp(a.in[T]) - L->c_out * a.old[T];
       a.out[T] = vN;
       alpha = sqrt((sx[2] + sy[2]) + vN * vN);
       L->alpha = alpha;
@@ -582,7 +640,6 @@ Mats make_mats(const Handle &H) {
   M.q = H.q; M.b = H.b; M.Pxbar = H.Pxbar; M.xbar = H.xbar; M.ybar = H.ybar; M.sbar = H.sbar;
   M.emb = H.emb;
   M.NX = H.NX; M.NY = H.NY;
-  M.gx = H.gx; M.gy = H.gy;
   M.dpi = H.cones.view();
   M.sP = H.sP.view(); M.sAT = H.sAT.view(); M.sA = H.sA.view();
   M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
@@ -637,10 +694,20 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
     kern<<<grid, threads, sm_bytes, st>>>(M, a);
   };
+  // the CTA-per-row path and the rarely used features run as their own
+  // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
+  // partitioned / rank-one steps the all-features one
+  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
   if (kind == STEP_F) {
-    if (minb == 12) go(k_step<STEP_F, 12>, 0); else go(k_step<STEP_F, 8>, 0);
+    if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
+    else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
+    else if (minb == 12) go(k_step<STEP_F, 12, 0>, 0);
+    else go(k_step<STEP_F, 8, 0>, 0);
   } else {
-    if (minb == 12) go(k_step<STEP_FT, 12>, smem); else go(k_step<STEP_FT, 8>, smem);
+    if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
+    else if (feat == kFeatWide) go(k_step<STEP_FT, 12, kFeatWide>, smem);
+    else if (minb == 12) go(k_step<STEP_FT, 12, 0>, smem);
+    else go(k_step<STEP_FT, 8, 0>, smem);
   }
   QG_LAUNCHED();
 }

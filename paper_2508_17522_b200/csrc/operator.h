@@ -8,7 +8,7 @@ namespace qg {
 
 enum StepKind { STEP_F = 0, STEP_FT = 1 };
 enum FinPhase { PH_APPLY = 0, PH_RHS = 1, PH_INIT_V = 2, PH_STEP_U = 3, PH_STEP_V = 4, PH_STEP_X = 5 };
-enum RhsKind { RHS_JVP = 0, RHS_VJP = 1 };
+enum RhsKind { RHS_JVP = 0, RHS_VJP = 1, RHS_VEC = 2 };
 
 struct StepArgs {
   const double *in;    // EVec, raw
@@ -27,6 +27,9 @@ struct StepArgs {
   double *upd_h = nullptr, *upd_hb = nullptr, *upd_x = nullptr;
   int xmode = X_FULL;         // row-partitioned mode phase (ops_dev.cuh)
   double *xred = nullptr;     // [NX] A' partials (X_PARTIAL writes, X_FINISH reads)
+  // rank-one term of the refine Jacobian J = F - r e_N' (testkit.py:443-451):
+  // F step out -= r w_N ; F' step T out -= r'w (dot partial in slot 3)
+  const double *rk1 = nullptr;
 };
 
 struct FinArgs {
@@ -43,6 +46,7 @@ struct FinArgs {
   // X-side and Y-side producers of this phase
   const double *px = nullptr, *py = nullptr;
   const int64_t *px_ptr = nullptr, *py_ptr = nullptr;
+  const double *rk1 = nullptr;  // rank-one term (StepArgs::rk1), T entries read here
 };
 
 struct UpdArgs {
@@ -79,7 +83,9 @@ void launch_vjp_grad(const Handle &H, const Mats &M, const double *w, double *dP
                      double *db, cudaStream_t st);
 void launch_embed_prep(const Handle &H, const double *x, const double *y, const double *s, double *zmid,
                        cudaStream_t st);
-void launch_embed_consts(const Handle &H, const Mats &M, double *part, cudaStream_t st);
+void launch_embed_consts(const Handle &H, const Mats &M, double *part, cudaStream_t st, const double *zT = nullptr);
+void launch_residual(const Handle &H, const Mats &M, double *out, double *part, cudaStream_t st);
+void launch_vec_rhs(const Handle &H, const Mats &M, const double *r, double *u, double *part, cudaStream_t st);
 void launch_csr_spmv(const int32_t *rp, const int32_t *col, const double *val, int64_t nrows, const double *x,
                      double *out, cudaStream_t st);
 void launch_kkt(const Handle &H, const Mats &M, const double *x, const double *y, const double *s,

@@ -16,7 +16,6 @@ struct Mats {
   const double *q, *b, *Pxbar, *xbar, *ybar, *sbar;
   const Embed *emb;
   int64_t NX, NY;
-  int gx, gy;
   DpiView dpi;
   SellView sP, sAT, sA;                 // SELL copies (MODE_SELL units)
   const int32_t *x_rowof, *y_rowof;     // lane -> row per slice (-1 = padding)
@@ -81,6 +80,33 @@ __device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, 
   }
   acc_a = a;
   acc_b = b;
+}
+
+// CTA-strided dot of one long CSR row (MODE_WIDE): thread t takes entries
+// t, t + blockDim, ... into 4 rotating partial sums, combined pairwise.
+__device__ __forceinline__ double wide_dot(const int32_t *rp, const int32_t *col, const double *val,
+                                           const double *vec, int r) {
+  const int k1 = rp[r + 1], step = (int)blockDim.x;
+  double a = 0.0, b = 0.0, c = 0.0, d = 0.0;
+  int k = rp[r] + (int)threadIdx.x;
+  for (; k + 3 * step < k1; k += 4 * step) {
+    a += __ldcs(val + k) * vec[__ldcs(col + k)];
+    b += __ldcs(val + k + step) * vec[__ldcs(col + k + step)];
+    c += __ldcs(val + k + 2 * step) * vec[__ldcs(col + k + 2 * step)];
+    d += __ldcs(val + k + 3 * step) * vec[__ldcs(col + k + 3 * step)];
+  }
+  for (; k < k1; k += step) a += __ldcs(val + k) * vec[__ldcs(col + k)];
+  return (a + b) + (c + d);
+}
+
+// Warp-per-row dot (G = 32), lane-strided in storage order per lane.
+__device__ __forceinline__ double row_dot32(const int32_t *rp, const int32_t *col, const double *val,
+                                            const double *vec, int r, int lane) {
+  double s = 0.0;
+  const int k1 = rp[r + 1];
+#pragma unroll 4
+  for (int k = rp[r] + lane; k < k1; k += 32) s += val[k] * vec[col[k]];
+  return s;
 }
 
 // Group-of-G sum inside a warp (G power of two, runtime).

@@ -85,12 +85,15 @@ struct Unit {
   int32_t row0, row1;
   int32_t blk0, blk1;
   int32_t cls;
-  int32_t mode;    // MODE_SELL: thread-per-row over SELL slices [s0, s1); MODE_LONG: warp-per-row CSR
+  int32_t mode;    // MODE_SELL: thread-per-row over SELL slices [s0, s1); MODE_LONG: G lanes per CSR
+                   // row; MODE_WIDE: the whole CTA per CSR row (rows of thousands of entries)
   int32_t s0, s1;
   int32_t group;   // SOC units: 1 = thread-per-block fused epilogue (dims <= 32); 0 = generic CTA path
+  int32_t lanes;   // CSR lanes per row for this unit's rows (power of two <= 32, from its mean row length)
 };
 
-enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1 };
+enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1, MODE_WIDE = 2 };
+constexpr int kWideRow = 512;   // mean entries per row from which a CSR unit goes CTA-per-row
 
 // A warp task of the SpMV steps: a pair of SELL slices (a, b; b = -1 if
 // none) or a range of long CSR rows [a, b) processed warp-per-row.  Tasks

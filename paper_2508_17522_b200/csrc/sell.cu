@@ -148,14 +148,30 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
   std::vector<int32_t> slice_pos, slice_n, slice_b1, slice_b2;
   int64_t ns = 0;
   const int max_row = allow_sell ? kSellMaxRow : -1;
+  static const char *env_wide = std::getenv("QG_WIDE_ROW");  // A/B: mean row length for MODE_WIDE
+  const int wide_row = env_wide ? std::atoi(env_wide) : kWideRow;
   for (auto &u : units) {
     int maxlen = 0;
+    int64_t total = 0, both = 0;
     for (int r = u.row0; r < u.row1; ++r) {
-      int len = rp1[r + 1] - rp1[r];
-      if (rp2) len = std::max(len, (*rp2)[r + 1] - (*rp2)[r]);
+      const int l1 = rp1[r + 1] - rp1[r], l2 = rp2 ? (*rp2)[r + 1] - (*rp2)[r] : 0;
+      const int len = std::max(l1, l2);
       maxlen = std::max(maxlen, len);
+      total += len;
+      both += l1 + l2;
+    }
+    // lanes per CSR row from THIS unit's mean row length: a side mixing a few
+    // dense rows with many short ones (C5b) must not run the short rows a
+    // warp each (measured 6x slower than per-unit lanes)
+    u.lanes = 1;
+    if (u.row1 > u.row0) {
+      const double avg = (double)both / (double)(u.row1 - u.row0);
+      while (u.lanes < 32 && u.lanes < avg * 0.75) u.lanes <<= 1;
     }
     u.mode = maxlen > max_row ? MODE_LONG : MODE_SELL;
+    // rows of thousands of entries (dense feature blocks, C5b): the whole CTA
+    // streams one row at a time instead of one warp per row
+    if (u.mode == MODE_LONG && u.row1 > u.row0 && total >= (int64_t)wide_row * (u.row1 - u.row0)) u.mode = MODE_WIDE;
     u.s0 = u.s1 = (int32_t)ns;
     if (u.mode == MODE_SELL) {
       for (int r = u.row0; r < u.row1; r += 32) {
@@ -270,6 +286,9 @@ void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<in
                           bx, by, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
                           &H.y_rowof, sy, bx, nullptr, st);
+  H.has_wide = false;
+  for (const auto *us : {&H.xunits, &H.cones.units})
+    for (const Unit &u : *us) H.has_wide = H.has_wide || u.mode == MODE_WIDE;
 }
 
 }  // namespace qg

@@ -309,6 +309,28 @@ class QCPBatch:
         N.check(N.lib().qg_embedding_point(self._h, N.ptr(out), N.stream_ptr()))
         return out
 
+    # -- re-solving oracle (testkit.refine / fd_jvp) --------------------------
+    def set_point_device(self, z, want_deriv=True):
+        """Move the handle to the embedding point ``z`` (CUDA, [X | Y | T])."""
+        N.check(N.lib().qg_set_point(self._h, N.ptr(z.contiguous()), 1 if want_deriv else 0, N.stream_ptr()))
+
+    def residual_device(self):
+        """Normalized residual N(z) at the handle's point (CUDA, [X | Y | T])."""
+        out = N.empty(self.NX + self.NY + self.B)
+        N.check(N.lib().qg_residual(self._h, N.ptr(out), N.stream_ptr()))
+        return out[:self.NX + self.NY + self.B]
+
+    def lsmr_jacobian_device(self, rhs, rank1=None, *, atol=1e-10, btol=1e-10, max_iter=None):
+        """LSMR on J = F - rank1 e_N' (F alone for rank1=None) at the handle's
+        point; returns (solution, diags)."""
+        sol = N.empty(self.NX + self.NY + self.B)
+        diags = (N.DiagC * self.B)()
+        o = _opts(atol, btol, max_iter)
+        N.check(N.lib().qg_lsmr_jacobian(self._h, N.ptr(rhs.contiguous()),
+                                         N.ptr(rank1.contiguous()) if rank1 is not None else None,
+                                         N.ctypes.byref(o), N.ptr(sol), diags, N.stream_ptr()))
+        return sol[:self.NX + self.NY + self.B], list(diags)
+
     def kkt_device(self, x=None, y=None, s=None):
         x0, y0, s0 = self._sol_dev
         rep = (N.c_dbl * (5 * self.B))()

@@ -142,6 +142,23 @@ def _validate(nrows, ncols, col_ptr, row_idx, values):
         raise ValidationError("matrix values must be finite")
 
 
+def add_scaled(a, b, alpha=1.0):
+    """``a + alpha * b`` on the union pattern, entries of a column in row
+    order, cancellations kept as explicit entries (reference sparse.py:142-170;
+    host-side construction of shifted problem data for fd_jvp)."""
+    if a.shape != b.shape:
+        raise ValidationError(f"cannot add matrices of shapes {a.shape} and {b.shape}")
+    stride = np.int64(max(a.nrows, 1))
+    keys = np.concatenate([a.entry_cols() * stride + a.row_idx, b.entry_cols() * stride + b.row_idx])
+    uniq, inv = np.unique(keys, return_inverse=True)
+    # per union entry: 0 + a_ij (+ alpha b_ij), in operand order
+    vals = np.bincount(inv, weights=np.concatenate([a.values, alpha * b.values]), minlength=uniq.size)
+    cols, rows = uniq // stride, uniq % stride
+    cp = np.zeros(a.ncols + 1, dtype=np.int64)
+    np.cumsum(np.bincount(cols, minlength=a.ncols), out=cp[1:])
+    return CscMatrix(a.nrows, a.ncols, cp, rows.astype(np.int64), vals)
+
+
 def same_pattern(a, b):
     return (a.shape == b.shape and (a.col_ptr is b.col_ptr or np.array_equal(a.col_ptr, b.col_ptr))
             and (a.row_idx is b.row_idx or np.array_equal(a.row_idx, b.row_idx)))
