@@ -230,6 +230,11 @@ def cone_struct(blocks):
 def cone_table(per_problem):
     """Concatenated cone table for a batch; lists shared between problems
     (the same list object) are converted once."""
+    if per_problem and all(bl is per_problem[0] for bl in per_problem):
+        # one shared block list (a homogeneous batch): tile it
+        one = cone_struct(per_problem[0])
+        return (np.ascontiguousarray(np.tile(one, len(per_problem))),
+                np.full(len(per_problem), len(one), dtype=np.int64))
     cache, parts = {}, []
     for bl in per_problem:
         arr = cache.get(id(bl))

@@ -36,6 +36,26 @@ cudaStream_t &alloc_stream() {
   return s;
 }
 
+void *pinned_staging(size_t bytes, int slot) {
+  struct Buf {
+    void *p = nullptr;
+    size_t n = 0;
+    ~Buf() {
+      if (p) cudaFreeHost(p);
+    }
+  };
+  static thread_local Buf bufs[4];
+  Buf &b = bufs[slot];
+  if (bytes > b.n) {
+    if (b.p) QG_CUDA(cudaFreeHost(b.p));
+    b.p = nullptr;
+    b.n = 0;
+    QG_CUDA(cudaMallocHost(&b.p, bytes));
+    b.n = bytes;
+  }
+  return b.p;
+}
+
 void init_pool() {
   static std::once_flag once;
   std::call_once(once, [] {
@@ -52,7 +72,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(part_t); dev_free(rk1);
+  dev_free(st); dev_free(d_nactive); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -80,7 +100,6 @@ Handle::~Handle() {
   sP.release(); sAT.release(); sA.release();
   dev_free(x_rowof); dev_free(y_rowof);
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
-  dev_free(d_tasks); dev_free(d_xt_ptr); dev_free(d_yt_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   dev_free(xred); dev_free(psum); dev_free(d_iota);
   ws.release();
@@ -144,11 +163,12 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     QG_CUDA(cudaMemcpyAsync(H.AT.val, d.A_vals, sizeof(double) * H.noffA[B], cudaMemcpyDeviceToDevice, st));
   trace("transpose A");
 
-  // row-length statistics for the group sizes and unit partition
-  std::vector<int32_t> rpP(H.NX + 1), rpAT(H.NX + 1), rpA(H.NY + 1);
-  QG_CUDA(cudaMemcpyAsync(rpP.data(), H.P.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
-  QG_CUDA(cudaMemcpyAsync(rpAT.data(), H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
-  QG_CUDA(cudaMemcpyAsync(rpA.data(), H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
+  // row-length statistics for the unit partition (pinned staging: DMA speed)
+  int32_t *rpP = static_cast<int32_t *>(pinned_staging(sizeof(int32_t) * (2 * (H.NX + 1) + H.NY + 1), 0));
+  int32_t *rpAT = rpP + (H.NX + 1), *rpA = rpAT + (H.NX + 1);
+  QG_CUDA(cudaMemcpyAsync(rpP, H.P.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpAT, H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpA, H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
   trace("rowptr D2H");
   const int64_t nnzX = (int64_t)rpP[H.NX] + rpAT[H.NX], nnzY = rpA[H.NY];
@@ -160,39 +180,43 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
   const int64_t target_rows_y = std::max<int64_t>(8, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
 
-  // X units: nnz-balanced row ranges within each problem
+  // X units: nnz-balanced row ranges within each problem (problems in
+  // parallel host chunks, concatenated in problem order)
   H.xunit_ptr.assign(B + 1, 0);
-  for (int p = 0; p < B; ++p) {
-    H.xunit_ptr[p] = (int64_t)H.xunits.size();
-    int64_t r = H.xoff[p];
-    const int64_t end = H.xoff[p + 1];
-    while (r < end) {
-      int64_t e = r, w = 0;
-      while (e < end && (e == r || (w < target_nnz && e - r < 4096))) {
-        w += (int64_t)(rpP[e + 1] - rpP[e]) + (rpAT[e + 1] - rpAT[e]) + 1;
-        ++e;
+  {
+    const int64_t nchunk = std::min<int64_t>(B, 64);
+    std::vector<std::vector<Unit>> part(nchunk);
+    host_parallel(nchunk, 1, [&](int64_t c0, int64_t c1) {
+      for (int64_t c = c0; c < c1; ++c) {
+        std::vector<Unit> &out = part[c];
+        for (int p = (int)(B * c / nchunk); p < (int)(B * (c + 1) / nchunk); ++p) {
+          H.xunit_ptr[p + 1] = 0;
+          int64_t r = H.xoff[p];
+          const int64_t end = H.xoff[p + 1];
+          while (r < end) {
+            int64_t e = r, w = 0;
+            while (e < end && (e == r || (w < target_nnz && e - r < 4096))) {
+              w += (int64_t)(rpP[e + 1] - rpP[e]) + (rpAT[e + 1] - rpAT[e]) + 1;
+              ++e;
+            }
+            out.push_back(Unit{p, (int32_t)r, (int32_t)e, 0, 0, CLS_ELEM});
+            ++H.xunit_ptr[p + 1];
+            r = e;
+          }
+        }
       }
-      H.xunits.push_back(Unit{p, (int32_t)r, (int32_t)e, 0, 0, CLS_ELEM});
-      r = e;
-    }
+    });
+    for (int p = 0; p < B; ++p) H.xunit_ptr[p + 1] += H.xunit_ptr[p];
+    H.xunits.reserve(H.xunit_ptr[B]);
+    for (auto &v : part) H.xunits.insert(H.xunits.end(), v.begin(), v.end());
   }
-  H.xunit_ptr[B] = (int64_t)H.xunits.size();
-  H.d_xunits = dev_alloc<Unit>(H.xunits.size());
-  if (!H.xunits.empty())
-    QG_CUDA(cudaMemcpyAsync(H.d_xunits, H.xunits.data(), sizeof(Unit) * H.xunits.size(), cudaMemcpyHostToDevice, st));
+  H.d_xunits = dev_alloc<Unit>(H.xunits.size());  // uploaded by build_sell with the modes
+  trace("x units");
 
   // cones and Y units
-  std::vector<std::vector<qg_cone_block>> per(B);
-  int64_t bi = 0;
-  for (int p = 0; p < B; ++p) {
-    per[p].assign(d.blocks + bi, d.blocks + bi + d.nblocks[p]);
-    bi += d.nblocks[p];
-  }
-  trace("x units");
-  H.cones.build(per, H.yoff, target_rows_y, st);
+  H.cones.build(d.blocks, d.nblocks, H.yoff, target_rows_y, st);
   trace("cone table");
   build_sell(H, rpP, rpAT, rpA, st);
-  build_tasks(H, st);
   trace("sell layout");
   H.d_xoff = dev_alloc<int64_t>(B + 1);
   H.d_yoff = dev_alloc<int64_t>(B + 1);
@@ -224,7 +248,6 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.dpu = dev_alloc<double>(H.NY); W.dpv = dev_alloc<double>(H.NY);
   W.tY = dev_alloc<double>(H.NY); W.tY2 = dev_alloc<double>(H.NY);
   W.part = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
-  W.part_t = dev_alloc<double>((size_t)(H.ntx + H.nty + 1) * kSlots);
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
   W.h_nactive = nullptr;
@@ -820,12 +843,10 @@ int qg_cones_create(qg_cones **out, const qg_cone_block *blocks, int64_t nblocks
   QG_API_BEGIN
   auto *c = new ConesHandle();
   try {
-    std::vector<std::vector<qg_cone_block>> per(1);
-    per[0].assign(blocks, blocks + nblocks);
     int64_t m = 0;
-    for (auto &b : per[0]) m += b.dim;
+    for (int64_t i = 0; i < nblocks; ++i) m += blocks[i].dim;
     std::vector<int64_t> yoff{0, m};
-    c->t.build(per, yoff, 1024, (cudaStream_t)stream);
+    c->t.build(blocks, &nblocks, yoff, 1024, (cudaStream_t)stream);
   } catch (...) {
     delete c;
     throw;

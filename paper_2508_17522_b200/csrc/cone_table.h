@@ -28,7 +28,8 @@ struct ConeTable {
   ConeTable &operator=(const ConeTable &) = delete;
   ~ConeTable();
 
-  void build(const std::vector<std::vector<qg_cone_block>> &per_prob, const std::vector<int64_t> &yoff,
+  // blocks: concatenated per problem, nblocks[p] of problem p (yoff: [nprob+1])
+  void build(const qg_cone_block *blocks, const int64_t *nblocks, const std::vector<int64_t> &yoff,
              int64_t target_rows, cudaStream_t st);
   // Projection of z (primal or dual) into proj (may be null) and, when
   // want_deriv, the derivative parameters at z (z is kept as zmid).

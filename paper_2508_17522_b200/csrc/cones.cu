@@ -221,78 +221,105 @@ void ConeTable::apply(const double *in, double *out, cudaStream_t st) {
   QG_LAUNCHED();
 }
 
-void ConeTable::build(const std::vector<std::vector<qg_cone_block>> &per_prob, const std::vector<int64_t> &yoff,
+void ConeTable::build(const qg_cone_block *blocks, const int64_t *nblocks, const std::vector<int64_t> &yoff,
                       int64_t target_rows, cudaStream_t st) {
-  nprob = (int)per_prob.size();
+  nprob = (int)yoff.size() - 1;
   ny = yoff.back();
-  int64_t nsoc = 0, ntri = 0, psd_total = 0;
+  // serial pass: validation and per-problem parameter offsets
+  std::vector<int64_t> boff(nprob + 1, 0), soc_off(nprob + 1, 0), tri_off(nprob + 1, 0), psd_off(nprob + 1, 0);
   for (int p = 0; p < nprob; ++p) {
-    int64_t row = yoff[p];
-    for (size_t i = 0; i < per_prob[p].size(); ++i) {
-      const qg_cone_block &c = per_prob[p][i];
-      BlockInfo b{};
-      b.kind = c.kind;
-      b.row = (int32_t)row;
-      b.dim = c.dim;
-      b.order = c.order;
-      b.alpha = c.alpha;
-      b.prob = p;
-      b.local = (int32_t)i;
-      b.param = -1;
-      if (c.kind == QG_CONE_SOC) b.param = nsoc++;
+    boff[p + 1] = boff[p] + nblocks[p];
+    int64_t rows = 0, ns = 0, nt = 0, np = 0;
+    for (int64_t i = boff[p]; i < boff[p + 1]; ++i) {
+      const qg_cone_block &c = blocks[i];
+      rows += c.dim;
+      if (c.kind == QG_CONE_SOC) ++ns;
       else if (c.kind == QG_CONE_PSD) {
         if (c.order > kMaxPsdOrder)
           throw Error{QG_ERR_UNSUPPORTED, "psd block order " + std::to_string(c.order) +
                                               " exceeds this build's limit " + std::to_string(kMaxPsdOrder)};
-        b.param = psd_total;
-        psd_total += 2LL * c.order * c.order;
+        np += 2LL * c.order * c.order;
         max_psd_order = std::max(max_psd_order, (int)c.order);
-      } else if (c.kind >= QG_CONE_EXP) b.param = ntri++;
-      h_blk.push_back(b);
-      row += c.dim;
+      } else if (c.kind >= QG_CONE_EXP) ++nt;
     }
-    if (row != yoff[p + 1]) throw Error{QG_ERR_VALIDATION, "cone dimension does not match m"};
+    if (rows != yoff[p + 1] - yoff[p]) throw Error{QG_ERR_VALIDATION, "cone dimension does not match m"};
+    soc_off[p + 1] = soc_off[p] + ns;
+    tri_off[p + 1] = tri_off[p] + nt;
+    psd_off[p + 1] = psd_off[p] + np;
   }
-  // work units: never cross problems or classes
+  const int64_t nsoc = soc_off[nprob], ntri = tri_off[nprob], psd_total = psd_off[nprob];
+  h_blk.resize(boff[nprob]);
+  // parallel pass over problem chunks: block records and work units (never
+  // crossing problems or classes), concatenated in problem order
   unit_ptr.assign(nprob + 1, 0);
-  int64_t bi = 0;
-  for (int p = 0; p < nprob; ++p) {
-    unit_ptr[p] = (int64_t)units.size();
-    const int64_t bend = bi + (int64_t)per_prob[p].size();
-    while (bi < bend) {
-      const BlockInfo &b = h_blk[bi];
-      if (b.kind == QG_CONE_ZERO || b.kind == QG_CONE_NONNEG) {
-        for (int64_t r = b.row; r < b.row + b.dim; r += target_rows)
-          units.push_back(Unit{p, (int32_t)r, (int32_t)std::min<int64_t>(r + target_rows, b.row + b.dim),
-                               (int32_t)bi, (int32_t)bi + 1, CLS_ELEM});
-        ++bi;
-      } else if (b.kind == QG_CONE_PSD) {
-        units.push_back(Unit{p, b.row, b.row + b.dim, (int32_t)bi, (int32_t)bi + 1, CLS_PSD});
-        ++bi;
-      } else {
-        const int cls = (b.kind == QG_CONE_SOC) ? CLS_SOC : CLS_TRI;
-        const int64_t maxblk = (cls == CLS_SOC) ? 16 * kWarps : kThreads;
-        int64_t e = bi, rows = 0;
-        while (e < bend && e - bi < maxblk) {
-          const BlockInfo &c = h_blk[e];
-          const int ccls = (c.kind == QG_CONE_SOC) ? CLS_SOC : (c.kind >= QG_CONE_EXP ? CLS_TRI : -1);
-          if (ccls != cls) break;
-          if (rows > 0 && rows + c.dim > target_rows) break;
-          rows += c.dim;
-          ++e;
+  const int64_t nchunk = std::min<int64_t>(nprob, 64);
+  std::vector<std::vector<Unit>> part(nchunk);
+  host_parallel(nchunk, 1, [&](int64_t c0, int64_t c1) {
+    for (int64_t c = c0; c < c1; ++c) {
+      std::vector<Unit> &out = part[c];
+      for (int p = (int)(nprob * c / nchunk); p < (int)(nprob * (c + 1) / nchunk); ++p) {
+        int64_t row = yoff[p], isoc = soc_off[p], itri = tri_off[p], ipsd = psd_off[p];
+        for (int64_t i = boff[p]; i < boff[p + 1]; ++i) {
+          const qg_cone_block &cb = blocks[i];
+          BlockInfo b{};
+          b.kind = cb.kind;
+          b.row = (int32_t)row;
+          b.dim = cb.dim;
+          b.order = cb.order;
+          b.alpha = cb.alpha;
+          b.prob = p;
+          b.local = (int32_t)(i - boff[p]);
+          b.param = -1;
+          if (cb.kind == QG_CONE_SOC) b.param = isoc++;
+          else if (cb.kind == QG_CONE_PSD) {
+            b.param = ipsd;
+            ipsd += 2LL * cb.order * cb.order;
+          } else if (cb.kind >= QG_CONE_EXP) b.param = itri++;
+          h_blk[i] = b;
+          row += cb.dim;
         }
-        Unit un{p, b.row, (int32_t)(b.row + rows), (int32_t)bi, (int32_t)e, cls};
-        if (cls == CLS_SOC) {  // thread-per-block fused epilogue for small SOC blocks
-          int maxdim = 0;
-          for (int64_t k = bi; k < e; ++k) maxdim = std::max(maxdim, (int)h_blk[k].dim);
-          un.group = maxdim <= 32 ? 1 : 0;
+        const size_t before = out.size();
+        int64_t bi = boff[p];
+        const int64_t bend = boff[p + 1];
+        while (bi < bend) {
+          const BlockInfo &b = h_blk[bi];
+          if (b.kind == QG_CONE_ZERO || b.kind == QG_CONE_NONNEG) {
+            for (int64_t r = b.row; r < b.row + b.dim; r += target_rows)
+              out.push_back(Unit{p, (int32_t)r, (int32_t)std::min<int64_t>(r + target_rows, b.row + b.dim),
+                                 (int32_t)bi, (int32_t)bi + 1, CLS_ELEM});
+            ++bi;
+          } else if (b.kind == QG_CONE_PSD) {
+            out.push_back(Unit{p, b.row, b.row + b.dim, (int32_t)bi, (int32_t)bi + 1, CLS_PSD});
+            ++bi;
+          } else {
+            const int cls = (b.kind == QG_CONE_SOC) ? CLS_SOC : CLS_TRI;
+            const int64_t maxblk = (cls == CLS_SOC) ? 16 * kWarps : kThreads;
+            int64_t e = bi, rows = 0;
+            while (e < bend && e - bi < maxblk) {
+              const BlockInfo &cc = h_blk[e];
+              const int ccls = (cc.kind == QG_CONE_SOC) ? CLS_SOC : (cc.kind >= QG_CONE_EXP ? CLS_TRI : -1);
+              if (ccls != cls) break;
+              if (rows > 0 && rows + cc.dim > target_rows) break;
+              rows += cc.dim;
+              ++e;
+            }
+            Unit un{p, b.row, (int32_t)(b.row + rows), (int32_t)bi, (int32_t)e, cls};
+            if (cls == CLS_SOC) {  // thread-per-block fused epilogue for small SOC blocks
+              int maxdim = 0;
+              for (int64_t k = bi; k < e; ++k) maxdim = std::max(maxdim, (int)h_blk[k].dim);
+              un.group = maxdim <= 32 ? 1 : 0;
+            }
+            out.push_back(un);
+            bi = e;
+          }
         }
-        units.push_back(un);
-        bi = e;
+        unit_ptr[p + 1] = (int64_t)(out.size() - before);
       }
     }
-  }
-  unit_ptr[nprob] = (int64_t)units.size();
+  });
+  for (int p = 0; p < nprob; ++p) unit_ptr[p + 1] += unit_ptr[p];
+  units.reserve(unit_ptr[nprob]);
+  for (auto &v : part) units.insert(units.end(), v.begin(), v.end());
   nblk = (int64_t)h_blk.size();
   d_blk = dev_alloc<BlockInfo>(h_blk.size());
   QG_CUDA(cudaMemcpyAsync(d_blk, h_blk.data(), sizeof(BlockInfo) * h_blk.size(), cudaMemcpyHostToDevice, st));

@@ -60,7 +60,6 @@ struct Workspace {
   double *u = nullptr, *v = nullptr, *h = nullptr, *hb = nullptr, *x = nullptr;  // EVec
   double *dpu = nullptr, *dpv = nullptr, *tY = nullptr, *tY2 = nullptr;          // Y
   double *part = nullptr;    // per work-unit partial sums (X units then Y units)
-  double *part_t = nullptr;  // per warp-task partial sums of the SpMV steps
   double *rk1 = nullptr;     // EVec: refine rank-one vector (allocated on first use)
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
@@ -82,11 +81,6 @@ struct Handle {
   int32_t *y_rowof = nullptr;
   int64_t nslice_x = 0, nslice_y = 0;
   bool has_wide = false;        // some unit runs CTA-per-row (MODE_WIDE)
-  std::vector<Task> tasks;      // X tasks [0, ntx) then Y tasks [ntx, ntx + nty)
-  std::vector<int64_t> xt_ptr, yt_ptr;   // [B+1] per-problem task ranges (global task index)
-  int64_t ntx = 0, nty = 0;
-  Task *d_tasks = nullptr;
-  int64_t *d_xt_ptr = nullptr, *d_yt_ptr = nullptr;
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;
@@ -127,9 +121,6 @@ void csc_to_csr(const CscBatch &in, DevCsr &out, DevCsr *csc_as_rows, bool keep_
 
 // SELL copies of P, A' (X units) and A (Y units); sets unit modes / slices
 // (sell.cu).  rp* are host copies of the CSR row pointers.
-void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
-                const std::vector<int32_t> &rpA, cudaStream_t st);
-// Warp tasks of the SpMV steps from the units' modes / slices (sell.cu).
-void build_tasks(Handle &H, cudaStream_t st);
+void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, cudaStream_t st);
 
 }  // namespace qg

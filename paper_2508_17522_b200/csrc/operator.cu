@@ -644,10 +644,6 @@ Mats make_mats(const Handle &H) {
   M.sP = H.sP.view(); M.sAT = H.sAT.view(); M.sA = H.sA.view();
   M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
   M.xoff = H.d_xoff; M.yoff = H.d_yoff;
-  M.tasks = H.d_tasks; M.ntx = H.ntx; M.nty = H.nty;
-  M.xt_ptr = H.d_xt_ptr; M.yt_ptr = H.d_yt_ptr;
-  M.part_t = H.ws.part_t;
-  M.part_u = H.ws.part;
   M.x_owner = H.x_owner() ? 1 : 0;
   return M;
 }

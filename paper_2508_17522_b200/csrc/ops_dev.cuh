@@ -20,11 +20,6 @@ struct Mats {
   SellView sP, sAT, sA;                 // SELL copies (MODE_SELL units)
   const int32_t *x_rowof, *y_rowof;     // lane -> row per slice (-1 = padding)
   const int64_t *xoff, *yoff;           // [B+1] problem offsets in X / Y
-  const Task *tasks;                    // warp tasks: X [0, ntx), Y [ntx, ntx + nty)
-  int64_t ntx, nty;
-  const int64_t *xt_ptr, *yt_ptr;       // [B+1] task ranges per problem
-  double *part_t;                       // per-task partial sums
-  double *part_u;                       // per-unit partial sums (X units then Y units)
   int x_owner;                          // 0: X rows are replicated and counted by rank 0 only
 };
 

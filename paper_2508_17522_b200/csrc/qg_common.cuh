@@ -11,7 +11,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qcpgrad.h"
@@ -95,14 +97,6 @@ struct Unit {
 enum UnitMode : int32_t { MODE_SELL = 0, MODE_LONG = 1, MODE_WIDE = 2 };
 constexpr int kWideRow = 512;   // mean entries per row from which a CSR unit goes CTA-per-row
 
-// A warp task of the SpMV steps: a pair of SELL slices (a, b; b = -1 if
-// none) or a range of long CSR rows [a, b) processed warp-per-row.  Tasks
-// never cross problems; one warp per task, no CTA-level synchronisation.
-enum TaskKind : int32_t { TASK_SELL = 0, TASK_LONG = 1 };
-struct Task {
-  int32_t prob, kind, a, b;
-};
-
 // SELL-C-sigma storage (C = 32 = warp width, sigma = the work unit): the rows
 // of a unit are sorted by length (descending) and cut into slices of 32; in
 // slice s entry k of lane l sits at off[s] + 32 k + l, so a warp reads 32
@@ -116,26 +110,33 @@ struct SellView {
                           // has < 65536 columns): 10 instead of 12 B per entry
 };
 
-struct Csr {
-  int32_t nrows = 0;
-  int64_t nnz = 0;
-  int32_t *rowptr = nullptr;  // nrows+1 (global rows)
-  int32_t *col = nullptr;     // global column indices
-  double *val = nullptr;
-  int32_t *perm = nullptr;    // CSR position -> CSC entry (transposes only)
-};
+// ------------------------------------------------------------ host utils --
+// fn(lo, hi) over [0, n) split across up to 16 host threads, at least
+// min_chunk items each (batch preparation loops over rows / blocks of
+// independent problems).  fn must not throw.
+template <class F>
+void host_parallel(int64_t n, int64_t min_chunk, F fn) {
+  const int64_t hw = std::max<int64_t>(1, (int64_t)std::thread::hardware_concurrency());
+  const int64_t T = std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(hw, 16), n / std::max<int64_t>(min_chunk, 1)));
+  if (T <= 1) {
+    fn((int64_t)0, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(T - 1);
+  for (int64_t t = 1; t < T; ++t) th.emplace_back(fn, n * t / T, n * (t + 1) / T);
+  fn((int64_t)0, n / T);
+  for (auto &x : th) x.join();
+}
+
+// Page-locked staging buffer of this host thread (grow-only): large
+// device<->host copies of batch preparation run at DMA speed.
+void *pinned_staging(size_t bytes, int slot);
 
 // ---------------------------------------------------------- device utils --
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-template <int G>
-__device__ __forceinline__ double group_sum(double v) {
-#pragma unroll
-  for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
   return v;
 }
 

@@ -141,37 +141,44 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
 // the slice metadata and the padded matrices.  Returns the number of slices.
 // cb1 / cb2: per-problem column base of matrix 1 / 2 (X or Y offsets) when
 // 16-bit local indices are used, else null.
-int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const std::vector<int32_t> &rp1,
-                   const std::vector<int32_t> *rp2, const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2,
-                   int32_t **rowof_out, bool allow_sell, const std::vector<int64_t> *cb1,
-                   const std::vector<int64_t> *cb2, cudaStream_t st) {
+int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const int32_t *rp1, const int32_t *rp2,
+                   const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2, int32_t **rowof_out,
+                   bool allow_sell, const std::vector<int64_t> *cb1, const std::vector<int64_t> *cb2,
+                   cudaStream_t st) {
   std::vector<int32_t> slice_pos, slice_n, slice_b1, slice_b2;
   int64_t ns = 0;
   const int max_row = allow_sell ? kSellMaxRow : -1;
   static const char *env_wide = std::getenv("QG_WIDE_ROW");  // A/B: mean row length for MODE_WIDE
   const int wide_row = env_wide ? std::atoi(env_wide) : kWideRow;
+  // per-unit row statistics (units in parallel host chunks)
+  host_parallel((int64_t)units.size(), 1024, [&](int64_t lo, int64_t hi) {
+    for (int64_t ui = lo; ui < hi; ++ui) {
+      Unit &u = units[ui];
+      int maxlen = 0;
+      int64_t total = 0, both = 0;
+      for (int r = u.row0; r < u.row1; ++r) {
+        const int l1 = rp1[r + 1] - rp1[r], l2 = rp2 ? rp2[r + 1] - rp2[r] : 0;
+        const int len = std::max(l1, l2);
+        maxlen = std::max(maxlen, len);
+        total += len;
+        both += l1 + l2;
+      }
+      // lanes per CSR row from THIS unit's mean row length: a side mixing a
+      // few dense rows with many short ones (C5b) must not run the short rows
+      // a warp each (measured 6x slower than per-unit lanes)
+      u.lanes = 1;
+      if (u.row1 > u.row0) {
+        const double avg = (double)both / (double)(u.row1 - u.row0);
+        while (u.lanes < 32 && u.lanes < avg * 0.75) u.lanes <<= 1;
+      }
+      u.mode = maxlen > max_row ? MODE_LONG : MODE_SELL;
+      // rows of thousands of entries (dense feature blocks, C5b): the whole
+      // CTA streams one row at a time instead of one warp per row
+      if (u.mode == MODE_LONG && u.row1 > u.row0 && total >= (int64_t)wide_row * (u.row1 - u.row0))
+        u.mode = MODE_WIDE;
+    }
+  });
   for (auto &u : units) {
-    int maxlen = 0;
-    int64_t total = 0, both = 0;
-    for (int r = u.row0; r < u.row1; ++r) {
-      const int l1 = rp1[r + 1] - rp1[r], l2 = rp2 ? (*rp2)[r + 1] - (*rp2)[r] : 0;
-      const int len = std::max(l1, l2);
-      maxlen = std::max(maxlen, len);
-      total += len;
-      both += l1 + l2;
-    }
-    // lanes per CSR row from THIS unit's mean row length: a side mixing a few
-    // dense rows with many short ones (C5b) must not run the short rows a
-    // warp each (measured 6x slower than per-unit lanes)
-    u.lanes = 1;
-    if (u.row1 > u.row0) {
-      const double avg = (double)both / (double)(u.row1 - u.row0);
-      while (u.lanes < 32 && u.lanes < avg * 0.75) u.lanes <<= 1;
-    }
-    u.mode = maxlen > max_row ? MODE_LONG : MODE_SELL;
-    // rows of thousands of entries (dense feature blocks, C5b): the whole CTA
-    // streams one row at a time instead of one warp per row
-    if (u.mode == MODE_LONG && u.row1 > u.row0 && total >= (int64_t)wide_row * (u.row1 - u.row0)) u.mode = MODE_WIDE;
     u.s0 = u.s1 = (int32_t)ns;
     if (u.mode == MODE_SELL) {
       for (int r = u.row0; r < u.row1; r += 32) {
@@ -228,41 +235,7 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
 
 }  // namespace
 
-void build_tasks(Handle &H, cudaStream_t st) {
-  constexpr int kLongRowsPerTask = 4;
-  H.tasks.clear();
-  auto side = [&](const std::vector<Unit> &units, std::vector<int64_t> &ptr) {
-    ptr.assign(H.B + 1, 0);
-    size_t ui = 0;
-    for (int p = 0; p < H.B; ++p) {
-      ptr[p] = (int64_t)H.tasks.size();
-      for (; ui < units.size() && units[ui].prob == p; ++ui) {
-        const Unit &u = units[ui];
-        if (u.mode == MODE_SELL) {
-          for (int s = u.s0; s < u.s1; s += 2) H.tasks.push_back(Task{p, TASK_SELL, s, s + 1 < u.s1 ? s + 1 : -1});
-        } else {
-          for (int r = u.row0; r < u.row1; r += kLongRowsPerTask)
-            H.tasks.push_back(Task{p, TASK_LONG, r, std::min(u.row1, r + kLongRowsPerTask)});
-        }
-      }
-    }
-    ptr[H.B] = (int64_t)H.tasks.size();
-  };
-  side(H.xunits, H.xt_ptr);
-  H.ntx = (int64_t)H.tasks.size();
-  side(H.cones.units, H.yt_ptr);
-  H.nty = (int64_t)H.tasks.size() - H.ntx;
-  H.d_tasks = dev_alloc<Task>(H.tasks.size());
-  H.d_xt_ptr = dev_alloc<int64_t>(H.B + 1);
-  H.d_yt_ptr = dev_alloc<int64_t>(H.B + 1);
-  if (!H.tasks.empty())
-    QG_CUDA(cudaMemcpyAsync(H.d_tasks, H.tasks.data(), sizeof(Task) * H.tasks.size(), cudaMemcpyHostToDevice, st));
-  QG_CUDA(cudaMemcpyAsync(H.d_xt_ptr, H.xt_ptr.data(), sizeof(int64_t) * (H.B + 1), cudaMemcpyHostToDevice, st));
-  QG_CUDA(cudaMemcpyAsync(H.d_yt_ptr, H.yt_ptr.data(), sizeof(int64_t) * (H.B + 1), cudaMemcpyHostToDevice, st));
-}
-
-void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<int32_t> &rpAT,
-                const std::vector<int32_t> &rpA, cudaStream_t st) {
+void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, cudaStream_t st) {
   // Thread-per-row SELL pays off when a side has many short rows: enough
   // slices to fill the GPU with warps and rows short enough that a thread's
   // serial chain stays short.  Otherwise the side keeps G-lanes-per-row CSR
@@ -282,7 +255,7 @@ void build_sell(Handle &H, const std::vector<int32_t> &rpP, const std::vector<in
   bool small = f16 ? std::atoi(f16) != 0 : false;
   for (int p = 0; p < H.B && small; ++p) small = H.n[p] < 65536 && H.m[p] < 65536;
   const auto *bx = small ? &H.xoff : nullptr, *by = small ? &H.yoff : nullptr;
-  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, &rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,
+  H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,
                           bx, by, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
                           &H.y_rowof, sy, bx, nullptr, st);
