@@ -325,7 +325,7 @@ def run_ours(args):
     peaks = _peaks()
     ach = ab["FT"] / (t_ft / 1e3) / 1e9
     sx, sy = b.layout()
-    spmv = "SELL-32" if sx and sy else ("SELL-32/CSR" if sx or sy else "CSR group-per-row")
+    spmv = "SELL-32" if sx and sy else ("SELL-32/CSR" if sx or sy else "CSR per-unit lanes / CTA-per-row")
     roof = {"kernel": f"k_step<FT> ({spmv} SpMV A,A',P + D Pi x2 epilogue)", "bound": "hbm",
             "achieved": round(ach, 1), "peak": peaks[0], "peak_source": peaks[1], "unit": "GB/s",
             "frac": round(ach / peaks[0], 4), "traffic": _traffic(args.config, ab["FT"]),

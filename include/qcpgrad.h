@@ -21,6 +21,11 @@
  *                                   dprojection(_dual).matvec (cones.py:926-963)
  *   qg_spmv_csc                  <- _kernels.spmv / spmv_adjoint backend slot
  *                                   (_kernels/__init__.py:23-50, _csc.pyx:17-50)
+ *   qg_set_point / qg_residual / <- testkit.refine internals: make_F at any z,
+ *   qg_lsmr_jacobian                normalized_residual, the Gauss-Newton model
+ *                                   solve (embedding.py:374-427; testkit.py:410-470)
+ *   qg_comm_* / qg_create_batch_dist  no counterpart (row-partitioned multi-GPU,
+ *                                   SURVEY.md §8(e))
  */
 #ifndef QCPGRAD_H
 #define QCPGRAD_H

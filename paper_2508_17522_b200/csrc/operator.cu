@@ -42,7 +42,8 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
                                          const double *v2, const double *x1, const double *x2, int G,
-                                         int64_t b1, int64_t b2, RowFn row) {
+                                         int64_t b1, int64_t b2, const double *vs1, const double *vs2,
+                                         RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
     // warps claim pairs of slices dynamically (balances uneven units)
@@ -58,8 +59,13 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
       double a1, b1v, a2 = 0.0, b2v = 0.0;
-      sell_dot2(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
-      if (S2) sell_dot2(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
+      // vs1 / vs2: the problem's input vectors staged in shared memory
+      if (vs1) sell_dot2_local(S1, s, sb, lane, vs1, (int)b1, a1, b1v);
+      else sell_dot2(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
+      if (S2) {
+        if (vs2) sell_dot2_local(*S2, s, sb, lane, vs2, (int)b2, a2, b2v);
+        else sell_dot2(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
+      }
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
     }
@@ -155,7 +161,7 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
 // 128-thread CTAs: more slice pairs per warp inside a unit (smaller tail at the
 // closing reduction) at the same register-limited occupancy (8 CTAs/SM).
 constexpr int kStepThreads = 128;
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
@@ -164,6 +170,7 @@ constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
+  constexpr bool kStage = (FEAT & kFeatStage) != 0;
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -193,12 +200,28 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
     }
   }
 
+  // kStage: the problem's input vectors go to shared memory once per CTA, so
+  // every SELL gather is an LDS instead of an L1/L2 round trip
+  const double *vx = nullptr, *vy = nullptr;
+  if (kStage && u.mode == MODE_SELL) {  // CTA-uniform
+    const int64_t xo = M.xoff[p], nx = M.xoff[p + 1] - xo;
+    for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) sm[i] = inX[xo + i];
+    vx = sm;
+    if (isx) {
+      const double *y2 = KIND == STEP_F ? a.dpin : inY;
+      const int64_t yo = M.yoff[p], ny = M.yoff[p + 1] - yo;
+      for (int64_t i = threadIdx.x; i < ny; i += blockDim.x) sm[nx + i] = y2[yo + i];
+      vy = sm + nx;
+    }
+    __syncthreads();
+  }
+
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
       for_rows<kWide>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
-               u.lanes, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
+               u.lanes, M.yoff[p], 0, nullptr, nullptr, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
     auto xrow = [&](int r, double s1, double s2) {
@@ -223,10 +246,10 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
              };
     if (kDist && a.xmode == X_FINISH)
       for_rows<kWide>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
+               M.xoff[p], 0, nullptr, nullptr, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
       for_rows<kWide>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
-               M.xoff[p], M.yoff[p], xrow);
+               M.xoff[p], M.yoff[p], vx, vy, xrow);
     if (kDist && !M.x_owner)
 #pragma unroll
       for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;  // replicated rows: rank 0 counts them
@@ -235,7 +258,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
       for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0,
+               M.xoff[p], 0, vx, nullptr,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
                  const double o2 = (-s) + wN * M.b[r];
@@ -249,7 +272,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
       for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0,
+               M.xoff[p], 0, vx, nullptr,
                [&](int r, double s, double) {
                  a.tY[r] = (s - wN * M.b[r]) - inY[r];
                  if (kRk1) acc[3] += a.rk1[M.NX + r] * inY[r];
@@ -693,15 +716,19 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   // the CTA-per-row path and the rarely used features run as their own
   // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
   // partitioned / rank-one steps the all-features one
-  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
+  // Staged variant: SELL handles whose problems' vectors fit (H.stage_bytes)
+  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : (H.stage_bytes ? kFeatStage : 0));
+  const size_t ssm = std::max(smem, H.stage_bytes);
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
     else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
+    else if (feat == kFeatStage) go(k_step<STEP_F, 8, kFeatStage>, ssm);
     else if (minb == 12) go(k_step<STEP_F, 12, 0>, 0);
     else go(k_step<STEP_F, 8, 0>, 0);
   } else {
     if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
     else if (feat == kFeatWide) go(k_step<STEP_FT, 12, kFeatWide>, smem);
+    else if (feat == kFeatStage) go(k_step<STEP_FT, 12, kFeatStage>, ssm);
     else if (minb == 12) go(k_step<STEP_FT, 12, 0>, smem);
     else go(k_step<STEP_FT, 8, 0>, smem);
   }

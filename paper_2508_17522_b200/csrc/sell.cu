@@ -91,20 +91,22 @@ __global__ void k_sell_fill(int64_t nslices, const int32_t *rowof, const int32_t
   const int k0 = r >= 0 ? rp[r] : 0, len = r >= 0 ? rp[r + 1] - k0 : 0;
   const int64_t o = off[s];
   const int width = w[s];
-  const int base = col16 ? cbase[s] : 0;
+  // padding: value 0 at the problem's first column (a valid local index 0,
+  // also for kernels that gather from a staged per-problem vector)
+  const int base = cbase ? cbase[s] : 0;
   for (int k = 0; k < width; ++k) {
     const int64_t pos = o + 32LL * k + lane;
     const bool in = k < len;
     val[pos] = in ? csr_val[k0 + k] : 0.0;
     if (col16) col16[pos] = in ? (uint16_t)(csr_col[k0 + k] - base) : (uint16_t)0;
-    else col[pos] = in ? csr_col[k0 + k] : 0;
+    else col[pos] = in ? csr_col[k0 + k] : base;
   }
 }
 
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_t *wsrc, const DevCsr &csr,
-                 const int32_t *d_cbase, cudaStream_t st) {
+                 const int32_t *d_cbase, bool use16, cudaStream_t st) {
   M.w = dev_alloc<int32_t>(nslices);
   QG_CUDA(cudaMemcpyAsync(M.w, wsrc, sizeof(int32_t) * nslices, cudaMemcpyDeviceToDevice, st));
   int64_t *w32 = dev_alloc<int64_t>(nslices);
@@ -124,7 +126,7 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
   QG_CUDA(cudaMemcpyAsync(&total, M.off + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
   M.entries = total;
-  if (d_cbase) M.col16 = dev_alloc<uint16_t>(total);
+  if (use16) M.col16 = dev_alloc<uint16_t>(total);
   else M.col = dev_alloc<int32_t>(total);
   M.val = dev_alloc<double>(total);
   if (total > 0) {
@@ -139,12 +141,12 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
 
 // Decide modes and slice ranges on the host, sort rows on the device, build
 // the slice metadata and the padded matrices.  Returns the number of slices.
-// cb1 / cb2: per-problem column base of matrix 1 / 2 (X or Y offsets) when
-// 16-bit local indices are used, else null.
+// cb1 / cb2: per-problem column base of matrix 1 / 2 (X or Y offsets): the
+// padding column, and the subtrahend of the 16-bit local indices (use16).
 int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const int32_t *rp1, const int32_t *rp2,
                    const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2, int32_t **rowof_out,
                    bool allow_sell, const std::vector<int64_t> *cb1, const std::vector<int64_t> *cb2,
-                   cudaStream_t st) {
+                   bool use16, cudaStream_t st) {
   std::vector<int32_t> slice_pos, slice_n, slice_b1, slice_b2;
   int64_t ns = 0;
   const int max_row = allow_sell ? kSellMaxRow : -1;
@@ -225,8 +227,8 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
     d_b2 = dev_alloc<int32_t>(ns);
     QG_CUDA(cudaMemcpyAsync(d_b2, slice_b2.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
   }
-  fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, st);
-  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, st);
+  fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, use16, st);
+  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, use16, st);
   QG_CUDA(cudaStreamSynchronize(st));
   dev_free(keys); dev_free(keys_s); dev_free(rows); dev_free(rows_s); dev_free(tmp);
   dev_free(d_pos); dev_free(d_n); dev_free(w1); dev_free(w2); dev_free(d_b1); dev_free(d_b2);
@@ -254,14 +256,25 @@ void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_
   const char *f16 = std::getenv("QG_SELL16");
   bool small = f16 ? std::atoi(f16) != 0 : false;
   for (int p = 0; p < H.B && small; ++p) small = H.n[p] < 65536 && H.m[p] < 65536;
-  const auto *bx = small ? &H.xoff : nullptr, *by = small ? &H.yoff : nullptr;
   H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,
-                          bx, by, st);
+                          &H.xoff, &H.yoff, small, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
-                          &H.y_rowof, sy, bx, nullptr, st);
+                          &H.y_rowof, sy, &H.xoff, nullptr, small, st);
   H.has_wide = false;
   for (const auto *us : {&H.xunits, &H.cones.units})
     for (const Unit &u : *us) H.has_wide = H.has_wide || u.mode == MODE_WIDE;
+  // Shared-memory staging of the per-problem vectors for SELL gathers (when
+  // the largest problem's X + Y vectors fit 24 KB and no PSD block needs the
+  // dynamic smem): opt-in with QG_STAGE=1.  Measured on c5a it LOSES (F 0.457
+  // -> 0.494 ms, F' 0.58 -> 0.88 ms: fewer resident CTAs, LDS bank conflicts,
+  // the staging pass itself) -- L1 already serves most gathers.
+  H.stage_bytes = 0;
+  const char *stage = std::getenv("QG_STAGE");
+  if ((H.nslice_x + H.nslice_y) > 0 && !H.has_wide && H.cones.max_psd_order == 0 && stage && std::atoi(stage)) {
+    int64_t mx = 0;
+    for (int p = 0; p < H.B; ++p) mx = std::max<int64_t>(mx, H.n[p] + H.m[p]);
+    if (mx * 8 <= 24 * 1024) H.stage_bytes = (size_t)std::max<int64_t>(mx, 1) * 8;
+  }
 }
 
 }  // namespace qg
