@@ -288,33 +288,39 @@ static void launch_sub(const double *a, const double *b, double *out, int64_t n,
 }
 
 // ----------------------------------------------------------- LSMR loop --
-struct LoopVecs {
-  int ku, kv;
-};
+// Step / finalize arguments of one LSMR iteration (u-step with the deferred
+// update of the previous iteration, v-step), shared by the graph and the
+// persistent paths.
+static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &fu, FinArgs &fv) {
+  Workspace &W = H.ws;
+  const int ku = jvp ? STEP_F : STEP_FT, kv = jvp ? STEP_FT : STEP_F;
+  const double *rk1 = H.use_rk1 ? W.rk1 : nullptr;
+  su = StepArgs{W.v, W.dpv, W.u, W.u, ku == STEP_FT ? W.dpu : nullptr, W.tY, W.tY2, W.st, 0, W.part};
+  su.upd_h = W.h;
+  su.upd_hb = W.hb;
+  su.upd_x = W.x;
+  su.rk1 = rk1;
+  fu = FinArgs{H.B, PH_STEP_U, ku, W.st, W.part, W.v, W.u, W.u, W.h, W.hb, W.x, W.v};
+  fu.rk1 = rk1;
+  sv = StepArgs{W.u, W.dpu, W.v, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 1, W.part};
+  sv.rk1 = rk1;
+  fv = FinArgs{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
+  fv.rk1 = rk1;
+}
 
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
-  Workspace &W = H.ws;
   const int ku = jvp ? STEP_F : STEP_FT, kv = jvp ? STEP_FT : STEP_F;
   // The vector update of iteration k (hbar, x, h) runs fused into the u-step
   // kernel of iteration k+1 (which streams v_k anyway), and its stopping
   // test runs at the head of that iteration's PH_STEP_U finalize; the last
   // iteration's update is flushed by lsmr_flush().  4 launches / iteration.
-  const double *rk1 = H.use_rk1 ? W.rk1 : nullptr;
+  StepArgs su, sv;
+  FinArgs fu, fv;
+  iter_args(H, jvp, su, sv, fu, fv);
   for (int i = 0; i < iters; ++i) {
-    StepArgs su{W.v, W.dpv, W.u, W.u, ku == STEP_FT ? W.dpu : nullptr, W.tY, W.tY2, W.st, 0, W.part};
-    su.upd_h = W.h;
-    su.upd_hb = W.hb;
-    su.upd_x = W.x;
-    su.rk1 = rk1;
     launch_step(H, M, ku, su, st);
-    FinArgs fu{H.B, PH_STEP_U, ku, W.st, W.part, W.v, W.u, W.u, W.h, W.hb, W.x, W.v};
-    fu.rk1 = rk1;
     launch_fin(H, M, fu, st);
-    StepArgs sv{W.u, W.dpu, W.v, W.v, kv == STEP_FT ? W.dpv : nullptr, W.tY, W.tY2, W.st, 1, W.part};
-    sv.rk1 = rk1;
     launch_step(H, M, kv, sv, st);
-    FinArgs fv{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
-    fv.rk1 = rk1;
     launch_fin(H, M, fv, st);
   }
 }
@@ -398,6 +404,7 @@ static int kernels_per_iter(const Handle &H) {
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
   Workspace &W = H.ws;
   long long done = 0;
+  const bool persistent = persistent_ok(H);
   while (true) {
     launch_count_active(H, st);
     int *pinned = pinned_word();
@@ -408,8 +415,16 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
     // 16 first (early convergence wastes little), then chunks of 64
     const long long want = done == 0 ? std::min<long long>(rem, 16) : rem;
     const int g = want >= 64 ? 64 : (want >= 16 ? 16 : (want >= 4 ? 4 : 1));
-    launch_iters(H, M, jvp, g, st);
-    if (!H.comm || H.comm->capturable()) count_launch(g * kernels_per_iter(H));  // else counted as launched
+    if (persistent) {
+      // one cooperative launch for all g iterations (counted as it launches)
+      StepArgs su, sv;
+      FinArgs fu, fv;
+      iter_args(H, jvp, su, sv, fu, fv);
+      launch_lsmr_persistent(H, M, jvp ? STEP_F : STEP_FT, su, sv, fu, fv, g, st);
+    } else {
+      launch_iters(H, M, jvp, g, st);
+      if (!H.comm || H.comm->capturable()) count_launch(g * kernels_per_iter(H));  // else counted as launched
+    }
     done += g;
   }
 }

@@ -11,9 +11,13 @@
 //   k_fin       stopping rules                                     (lsmr.py:173-182)
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
+#include <cooperative_groups.h>
+
 #include "dpi_dev.cuh"
 #include "ops_dev.cuh"
 #include "operator.h"
+
+namespace cg = cooperative_groups;
 
 namespace qg {
 
@@ -167,15 +171,17 @@ constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
 // a.rk1 is set).  The common variant (0) carries none of them.
-template <int KIND, int MINB, int FEAT>
-__global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
+// One work unit (`ui`: X units then Y units) of an operator step, by the
+// whole CTA; the partial-sum slot of the unit is part[ui].
+template <int KIND, int FEAT>
+__device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
   constexpr bool kStage = (FEAT & kFeatStage) != 0;
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
-  const bool isx = (int)blockIdx.x < M.nxu;
-  const Unit u = isx ? M.xu[blockIdx.x] : M.yu[blockIdx.x - M.nxu];
+  const bool isx = ui < M.nxu;
+  const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];
   const int p = u.prob;
   double s_in, c_out;
   if (!lsmr_runs(a, p, s_in, c_out)) return;  // CTA-uniform
@@ -328,7 +334,12 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
   cta_sum_slots(acc, red, tot);
   if (threadIdx.x == 0 && a.part)
 #pragma unroll
-    for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
+}
+
+template <int KIND, int MINB, int FEAT>
+__global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
+  step_unit<KIND, FEAT>(M, a, (int)blockIdx.x);
 }
 
 // -------------------------------------------------------------- update --
@@ -438,10 +449,8 @@ __global__ void k_part_reduce(const double *px, const int64_t *px_ptr, const dou
     }
 }
 
-__global__ void k_fin(Mats M, FinArgs a) {
-  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int lane = threadIdx.x & 31;
-  if (p >= a.B) return;
+// Finalize of problem p by one warp (all 32 lanes call it).
+__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane) {
   Lsmr *L = a.st ? a.st + p : nullptr;
   if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
   if (L && a.phase == PH_STEP_V && L->skip_v) {
@@ -629,6 +638,47 @@ __global__ void k_fin(Mats M, FinArgs a) {
   if (a.phase == PH_STEP_X) stop_test(L, sx[0] + sy[0], a.x[T]);
 }
 
+__global__ void k_fin(Mats M, FinArgs a) {
+  const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (p < a.B) fin_problem(M, a, p, threadIdx.x & 31);
+}
+
+// Persistent LSMR for small batches (launch latency, not bandwidth, bounds
+// them): ONE cooperative launch runs `iters` iterations -- u-step over all
+// units, grid barrier, finalize (one warp per problem), barrier, v-step,
+// barrier, finalize, barrier -- the same device code as the 4-launch
+// graph path, so the arithmetic (and the results) are identical.
+struct LoopArgs {
+  StepArgs su, sv;
+  FinArgs fu, fv;
+  int iters;
+};
+
+template <int KU, int KV>
+__global__ void __launch_bounds__(kStepThreads, 4) k_lsmr_loop(Mats M, LoopArgs L) {
+  cg::grid_group grid = cg::this_grid();
+  const int nunits = M.nxu + M.nyu;
+  const int lane = threadIdx.x & 31;
+  const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
+  for (int it = 0; it < L.iters; ++it) {
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      step_unit<KU, 0>(M, L.su, u);
+      __syncthreads();
+    }
+    grid.sync();
+    for (int p = gw; p < L.fu.B; p += nw) fin_problem(M, L.fu, p, lane);
+    grid.sync();
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+      step_unit<KV, 0>(M, L.sv, u);
+      __syncthreads();
+    }
+    grid.sync();
+    for (int p = gw; p < L.fv.B; p += nw) fin_problem(M, L.fv, p, lane);
+    grid.sync();
+  }
+}
+
 __global__ void k_count_active(const Lsmr *st, int B, int *out) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
@@ -753,6 +803,45 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
     a.px_ptr = a.py_ptr = H.d_iota;
   }
   k_fin<<<grid, 256, 0, st>>>(M, a);
+  QG_LAUNCHED();
+}
+
+// The persistent loop applies to plain whole-problem handles (no row
+// partition, rank-one term, CTA-per-row units or staging) and is opt-in
+// (QG_PERSIST=1).  Measured per jvp+vjp step at K=100 (graph path -> persistent):
+// c1 7.8 -> 11.4 ms, c2 11.1 -> 20.2, c3 23.2 -> 43.7, c4 50.6 -> 47.1.  The
+// small configs are bound by each step's own dependent-load latency, not by
+// launches, and four grid barriers per iteration cost more than four graph
+// kernel nodes.
+bool persistent_ok(const Handle &H) {
+  if (H.comm || H.use_rk1 || H.has_wide || H.stage_bytes) return false;
+  static const char *env = std::getenv("QG_PERSIST");
+  return env && std::atoi(env) != 0;
+}
+
+void launch_lsmr_persistent(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
+                            const FinArgs &fu0, const FinArgs &fv0, int iters, cudaStream_t st) {
+  LoopArgs L{su, sv, fu0, fv0, iters};
+  for (FinArgs *f : {&L.fu, &L.fv}) {
+    f->px = H.ws.part;
+    f->px_ptr = H.d_xunit_ptr;
+    f->py = H.ws.part + (size_t)H.nxu() * kSlots;
+    f->py_ptr = H.d_yunit_ptr;
+  }
+  const size_t smem = step_smem(H);
+  void *kern = ku == STEP_F ? (void *)k_lsmr_loop<STEP_F, STEP_FT> : (void *)k_lsmr_loop<STEP_FT, STEP_F>;
+  if (smem > 48 * 1024)
+    QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0, per_sm = 0;
+  QG_CUDA(cudaGetDevice(&dev));
+  QG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  QG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem));
+  if (per_sm < 1) throw Error{QG_ERR_CUDA, "persistent LSMR kernel does not fit an SM"};
+  const int64_t want = std::max<int64_t>(std::max<int64_t>(H.nxu() + H.nyu(), (H.B + 3) / 4), 1);
+  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)per_sm * sms);
+  Mats m = M;
+  void *args[] = {&m, &L};
+  QG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kStepThreads), args, smem, st));
   QG_LAUNCHED();
 }
 

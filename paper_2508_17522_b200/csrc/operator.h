@@ -60,6 +60,11 @@ Mats make_mats(const Handle &H);
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
+// Persistent cooperative LSMR loop (small batches): eligibility, and one
+// launch running `iters` iterations with the given step / finalize arguments.
+bool persistent_ok(const Handle &H);
+void launch_lsmr_persistent(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
+                            const FinArgs &fu, const FinArgs &fv, int iters, cudaStream_t st);
 void launch_count_active(const Handle &H, cudaStream_t st);
 void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st);
 
