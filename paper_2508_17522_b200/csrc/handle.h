@@ -63,6 +63,7 @@ struct Workspace {
   double *rk1 = nullptr;     // EVec: refine rank-one vector (allocated on first use)
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
+  int *done = nullptr;       // [B] per-problem arrival counters of the fused finalize (kept 0)
   int *h_nactive = nullptr;  // pinned
   void release();
 };

@@ -165,18 +165,21 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
 // 128-thread CTAs: more slice pairs per warp inside a unit (smaller tail at the
 // closing reduction) at the same register-limited occupancy (8 CTAs/SM).
 constexpr int kStepThreads = 128;
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
+
+__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane);
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
-// a.rk1 is set).  The common variant (0) carries none of them.
+// a.rk1 is set), kFeatStage (smem-staged gathers), kFeatFin (fused finalize).
+// The common variant (0) carries none of them.
 // One work unit (`ui`: X units then Y units) of an operator step, by the
 // whole CTA; the partial-sum slot of the unit is part[ui].
 template <int KIND, int FEAT>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
-  constexpr bool kStage = (FEAT & kFeatStage) != 0;
+  constexpr bool kStage = (FEAT & kFeatStage) != 0, kFin = (FEAT & kFeatFin) != 0;
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -184,7 +187,15 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];
   const int p = u.prob;
   double s_in, c_out;
-  if (!lsmr_runs(a, p, s_in, c_out)) return;  // CTA-uniform
+  if (!lsmr_runs(a, p, s_in, c_out)) {  // CTA-uniform
+    // a skipped v-step (beta = 0) still runs its finalize recurrences
+    // (k_fin PH_STEP_V): the problem's first unit does it, no partials needed
+    if (kFin && a.is_v_step && a.st[p].active && a.st[p].skip_v && threadIdx.x < 32) {
+      const int first = M.xu_ptr[p] < M.xu_ptr[p + 1] ? (int)M.xu_ptr[p] : M.nxu + (int)M.yu_ptr[p];
+      if (ui == first) fin_problem(M, a.fin, p, (int)threadIdx.x);
+    }
+    return;
+  }
   const Embed E = M.emb[p];
   const double *inX = a.in, *inY = a.in + M.NX;
   const double wN = a.in[M.NX + M.NY + p];
@@ -335,6 +346,23 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   if (threadIdx.x == 0 && a.part)
 #pragma unroll
     for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
+  if (kFin) {
+    // last CTA of problem p to finish runs its finalize (threadFenceReduction
+    // pattern); the slot sums stay in k_fin's fixed order
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const int total = (int)(M.xu_ptr[p + 1] - M.xu_ptr[p] + M.yu_ptr[p + 1] - M.yu_ptr[p]);
+      const int prev = atomicAdd(a.done + p, 1);
+      s_last = prev == total - 1;
+      if (s_last) a.done[p] = 0;  // every unit of p has arrived: reset for the next step
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x < 32) {
+      __threadfence();
+      fin_problem(M, a.fin, p, (int)threadIdx.x);
+    }
+  }
 }
 
 template <int KIND, int MINB, int FEAT>
@@ -451,6 +479,8 @@ __global__ void k_part_reduce(const double *px, const int64_t *px_ptr, const dou
 
 // Finalize of problem p by one warp (all 32 lanes call it).
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane) {
+  // partials are read L2-coherent (__ldcg): in the fused variant they were
+  // written by other CTAs of the same launch
   Lsmr *L = a.st ? a.st + p : nullptr;
   if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
   if (L && a.phase == PH_STEP_V && L->skip_v) {
@@ -460,10 +490,10 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
   double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
   for (int64_t k = a.px_ptr[p] + lane; k < a.px_ptr[p + 1]; k += 32)
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sx[j] += a.px[k * kSlots + j];
+    for (int j = 0; j < kSlots; ++j) sx[j] += __ldcg(a.px + k * kSlots + j);
   for (int64_t k = a.py_ptr[p] + lane; k < a.py_ptr[p + 1]; k += 32)
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sy[j] += a.py[k * kSlots + j];
+    for (int j = 0; j < kSlots; ++j) sy[j] += __ldcg(a.py + k * kSlots + j);
 #pragma unroll
   for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
   if (lane != 0) return;
@@ -767,30 +797,38 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
   // partitioned / rank-one steps the all-features one
   // Staged variant: SELL handles whose problems' vectors fit (H.stage_bytes)
+  // Fused finalize (a.done set by the loop driver: whole-problem handles, no
+  // rank-one term, no staging): its own plain / wide variants.
   const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : (H.stage_bytes ? kFeatStage : 0));
   const size_t ssm = std::max(smem, H.stage_bytes);
+  const bool fin = a.done != nullptr && (feat == 0 || feat == kFeatWide);
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
-    else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
+    else if (feat == kFeatWide) fin ? go(k_step<STEP_F, 12, kFeatWide | kFeatFin>, 0) : go(k_step<STEP_F, 12, kFeatWide>, 0);
     else if (feat == kFeatStage) go(k_step<STEP_F, 8, kFeatStage>, ssm);
-    else if (minb == 12) go(k_step<STEP_F, 12, 0>, 0);
-    else go(k_step<STEP_F, 8, 0>, 0);
+    else if (minb == 12) fin ? go(k_step<STEP_F, 12, kFeatFin>, 0) : go(k_step<STEP_F, 12, 0>, 0);
+    else fin ? go(k_step<STEP_F, 8, kFeatFin>, 0) : go(k_step<STEP_F, 8, 0>, 0);
   } else {
     if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
-    else if (feat == kFeatWide) go(k_step<STEP_FT, 12, kFeatWide>, smem);
+    else if (feat == kFeatWide) fin ? go(k_step<STEP_FT, 12, kFeatWide | kFeatFin>, smem) : go(k_step<STEP_FT, 12, kFeatWide>, smem);
     else if (feat == kFeatStage) go(k_step<STEP_FT, 12, kFeatStage>, ssm);
-    else if (minb == 12) go(k_step<STEP_FT, 12, 0>, smem);
-    else go(k_step<STEP_FT, 8, 0>, smem);
+    else if (minb == 12) fin ? go(k_step<STEP_FT, 12, kFeatFin>, smem) : go(k_step<STEP_FT, 12, 0>, smem);
+    else fin ? go(k_step<STEP_FT, 8, kFeatFin>, smem) : go(k_step<STEP_FT, 8, 0>, smem);
   }
   QG_LAUNCHED();
 }
 
-void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
-  FinArgs a = a0;  // every producer writes one slot per work unit: X units, then Y units
+void fin_ptrs(const Handle &H, FinArgs &a) {
+  // every producer writes one slot per work unit: X units, then Y units
   a.px = H.ws.part;
   a.px_ptr = H.d_xunit_ptr;
   a.py = H.ws.part + (size_t)H.nxu() * kSlots;
   a.py_ptr = H.d_yunit_ptr;
+}
+
+void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
+  FinArgs a = a0;
+  fin_ptrs(H, a);
   const unsigned grid = (unsigned)((H.B * 32 + 255) / 256);
   if (H.comm) {
     // row-partitioned: per-problem sums (k_fin's order), summed over ranks,

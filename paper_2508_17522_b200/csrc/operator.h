@@ -10,6 +10,23 @@ enum StepKind { STEP_F = 0, STEP_FT = 1 };
 enum FinPhase { PH_APPLY = 0, PH_RHS = 1, PH_INIT_V = 2, PH_STEP_U = 3, PH_STEP_V = 4, PH_STEP_X = 5 };
 enum RhsKind { RHS_JVP = 0, RHS_VJP = 1, RHS_VEC = 2 };
 
+struct FinArgs {
+  int B;
+  int phase;
+  int kind;            // STEP_F / STEP_FT (or RhsKind for PH_RHS)
+  Lsmr *st;
+  const double *part;
+  const double *in;    // EVec (T component read)
+  const double *old;   // EVec
+  double *out;         // EVec (T component written)
+  double *h, *hb, *x, *v;
+  // filled by launch_fin: partial-sum arrays and per-problem ranges of the
+  // X-side and Y-side producers of this phase
+  const double *px = nullptr, *py = nullptr;
+  const int64_t *px_ptr = nullptr, *py_ptr = nullptr;
+  const double *rk1 = nullptr;  // rank-one term (StepArgs::rk1), T entries read here
+};
+
 struct StepArgs {
   const double *in;    // EVec, raw
   const double *dpin;  // Y: D Pi applied to in_Y (F step)
@@ -30,23 +47,11 @@ struct StepArgs {
   // rank-one term of the refine Jacobian J = F - r e_N' (testkit.py:443-451):
   // F step out -= r w_N ; F' step T out -= r'w (dot partial in slot 3)
   const double *rk1 = nullptr;
-};
-
-struct FinArgs {
-  int B;
-  int phase;
-  int kind;            // STEP_F / STEP_FT (or RhsKind for PH_RHS)
-  Lsmr *st;
-  const double *part;
-  const double *in;    // EVec (T component read)
-  const double *old;   // EVec
-  double *out;         // EVec (T component written)
-  double *h, *hb, *x, *v;
-  // filled by launch_fin: partial-sum arrays and per-problem ranges of the
-  // X-side and Y-side producers of this phase
-  const double *px = nullptr, *py = nullptr;
-  const int64_t *px_ptr = nullptr, *py_ptr = nullptr;
-  const double *rk1 = nullptr;  // rank-one term (StepArgs::rk1), T entries read here
+  // fused finalize: the last CTA of each problem (per-problem arrival counter
+  // `done`) runs that problem's finalize `fin` at the end of the step --
+  // 2 instead of 4 dependent launches per LSMR iteration
+  int *done = nullptr;
+  FinArgs fin{};
 };
 
 struct UpdArgs {
@@ -59,6 +64,7 @@ struct UpdArgs {
 Mats make_mats(const Handle &H);
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
+void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole-problem handle
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
 // Persistent cooperative LSMR loop (small batches): eligibility, and one
 // launch running `iters` iterations with the given step / finalize arguments.
