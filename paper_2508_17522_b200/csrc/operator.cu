@@ -41,7 +41,7 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 // receives the row sums of the one or two matrices (second may be unused).
 // WIDE: compile the CTA-per-row path (MODE_WIDE units exist); kept out of the
 // common kernels, whose SELL loops lose ~15% to its extra shared state.
-template <bool WIDE, class RowFn>
+template <bool WIDE, int UNR, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
@@ -65,10 +65,10 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       double a1, b1v, a2 = 0.0, b2v = 0.0;
       // vs1 / vs2: the problem's input vectors staged in shared memory
       if (vs1) sell_dot2_local(S1, s, sb, lane, vs1, (int)b1, a1, b1v);
-      else sell_dot2(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
+      else sell_dot2<UNR>(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
       if (S2) {
         if (vs2) sell_dot2_local(*S2, s, sb, lane, vs2, (int)b2, a2, b2v);
-        else sell_dot2(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
+        else sell_dot2<UNR>(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
       }
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
@@ -165,6 +165,12 @@ __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, c
 // 128-thread CTAs: more slice pairs per warp inside a unit (smaller tail at the
 // closing reduction) at the same register-limited occupancy (8 CTAs/SM).
 constexpr int kStepThreads = 128;
+#ifndef QG_F_UNROLL
+#define QG_F_UNROLL 4
+#endif
+#ifndef QG_FT_UNROLL
+#define QG_FT_UNROLL 2
+#endif
 constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
@@ -180,6 +186,7 @@ template <int KIND, int FEAT>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
   constexpr bool kStage = (FEAT & kFeatStage) != 0, kFin = (FEAT & kFeatFin) != 0;
+  constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -237,7 +244,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
-      for_rows<kWide>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
+      for_rows<kWide, kUnr>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
                u.lanes, M.yoff[p], 0, nullptr, nullptr, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
@@ -262,10 +269,10 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                acc[2] += o * o;
              };
     if (kDist && a.xmode == X_FINISH)
-      for_rows<kWide>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, nullptr, nullptr, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
-      for_rows<kWide>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
+      for_rows<kWide, kUnr>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
                M.xoff[p], M.yoff[p], vx, vy, xrow);
     if (kDist && !M.x_owner)
 #pragma unroll
@@ -274,7 +281,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
-      for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, vx, nullptr,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
@@ -288,7 +295,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                });
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
-      for_rows<kWide>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, vx, nullptr,
                [&](int r, double s, double) {
                  a.tY[r] = (s - wN * M.b[r]) - inY[r];

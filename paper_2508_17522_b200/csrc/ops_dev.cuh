@@ -53,19 +53,23 @@ __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
 // Two slices of one matrix at once (independent load streams -> twice the
 // memory-level parallelism per warp); slice b may be absent (sb < 0).  Each
 // lane's sums stay in storage order.
-template <class Idx>
+// UNR: unroll of the entry loop.  Measured on c5a (ms, F / F'): 2 -> 0.520 /
+// 0.527, 4 -> 0.454 / 0.574, 8 -> 0.563 / 0.588: the F step wants 4, the F'
+// step (which also carries the epilogue at 40 registers) wants 2.
+template <int UNR, class Idx>
 __device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *col, int64_t sa, int64_t sb, int lane,
                                             const double *vec, double &acc_a, double &acc_b);
 
 // Dispatch on the index width: 16-bit problem-local indices gather from
 // vec_local (= vec + this problem's column base), 32-bit global ones from vec.
+template <int UNR>
 __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t sb, int lane, const double *vec,
                                           const double *vec_local, double &acc_a, double &acc_b) {
-  if (S.col16) sell_dot2_t(S, S.col16, sa, sb, lane, vec_local, acc_a, acc_b);
-  else sell_dot2_t(S, S.col, sa, sb, lane, vec, acc_a, acc_b);
+  if (S.col16) sell_dot2_t<UNR>(S, S.col16, sa, sb, lane, vec_local, acc_a, acc_b);
+  else sell_dot2_t<UNR>(S, S.col, sa, sb, lane, vec, acc_a, acc_b);
 }
 
-template <class Idx>
+template <int UNR, class Idx>
 __device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, int64_t sa, int64_t sb, int lane,
                                             const double *vec, double &acc_a, double &acc_b) {
   const int64_t oa = S.off[sa] + lane;
@@ -75,7 +79,7 @@ __device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, 
   const int wm = wa < wb ? wa : wb;
   double a = 0.0, b = 0.0;
   int k = 0;
-#pragma unroll 4
+#pragma unroll UNR
   for (; k < wm; ++k) {
     const int64_t pa = oa + 32LL * k, pb = ob + 32LL * k;
     const double va = ld_stream(S.val + pa), vb = ld_stream(S.val + pb);
