@@ -300,6 +300,10 @@ def run_ours(args):
                 for k in ("dP", "dA", "dq", "db", "dx", "dy", "ds")}
         outs = {}
 
+        # whole-batch host path; pipeline.evaluate_host (chunked, copies on a
+        # second stream) measured slower on c5a: 324 / 353 ms at 1 / 4 chunks vs
+        # 307 ms -- the library's small preparation copies queue behind the
+        # next chunk's upload in the copy engine
         def step_host():
             outs.clear()  # release last step's pinned result buffers back to torch's host cache
             b = QCPBatch.from_host(*sizes, pin, comm=comm)
@@ -315,7 +319,8 @@ def run_ours(args):
             v.numel() * v.element_size() for v in pdir.values())
         d2h = 8 * (sum(bt.n) * 2 + sum(bt.m) * 3 + bt.P_vals.size + bt.A_vals.size)
         e2e = {"value": units_total / (ems / 1e3), "unit": "evals/s", "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": ems}
+               "d2h_bytes_per_step": int(d2h * world), "ms_per_step": ems,
+               "api": "QCPBatch.from_host + jvp_host + vjp_host (pinned host buffers)"}
 
     # roofline of the fused kernels (CUDA events inside the library, same stream)
     b = step_device()
