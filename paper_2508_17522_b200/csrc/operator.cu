@@ -171,7 +171,7 @@ constexpr int kStepThreads = 128;
 #ifndef QG_FT_UNROLL
 #define QG_FT_UNROLL 2
 #endif
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16, kFeatTyS = 32;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane);
@@ -186,6 +186,7 @@ template <int KIND, int FEAT>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
   constexpr bool kStage = (FEAT & kFeatStage) != 0, kFin = (FEAT & kFeatFin) != 0;
+  constexpr bool kTyS = (FEAT & kFeatTyS) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
@@ -294,11 +295,15 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                  acc[2] += o * o;
                });
     } else {
-      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
+      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit; kTyS keeps
+      // t in shared memory (rows [row0, row1) at sm[0..)) instead of an HBM
+      // round trip -- handles whose Y units all take the register / thread-
+      // per-block epilogues (no PSD, SOC dims <= 32)
+      double *tY = kTyS ? (sm - u.row0) : a.tY;
       for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, vx, nullptr,
                [&](int r, double s, double) {
-                 a.tY[r] = (s - wN * M.b[r]) - inY[r];
+                 tY[r] = (s - wN * M.b[r]) - inY[r];
                  if (kRk1) acc[3] += a.rk1[M.NX + r] * inY[r];
                });
       __syncthreads();
@@ -316,7 +321,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
         const int kind = M.dpi.blk[u.blk0].kind;
         for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
           const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
-          const double o = fin_row(r, wgt * a.tY[r]);
+          const double o = fin_row(r, wgt * tY[r]);
           if (a.dpout) a.dpout[r] = wgt * o;
         }
       } else if (u.cls == CLS_TRI) {
@@ -326,7 +331,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
 #pragma unroll
           for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
           const int flip = M.dpi.tri_flip[b.param];
-          const double t3[3] = {a.tY[b.row], a.tY[b.row + 1], a.tY[b.row + 2]};
+          const double t3[3] = {tY[b.row], tY[b.row + 1], tY[b.row + 2]};
           double r3[3], o3[3], d3[3];
           tri_apply(D, flip, t3, r3);
 #pragma unroll
@@ -338,7 +343,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
           }
         }
       } else if (u.cls == CLS_SOC && u.group > 0) {
-        soc_epilogue(M.dpi, u, a.tY, fin_row, outY, a.dpout);
+        soc_epilogue(M.dpi, u, tY, fin_row, outY, a.dpout);
       } else {
         // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
         dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
@@ -819,6 +824,7 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
     if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
     else if (feat == kFeatWide) fin ? go(k_step<STEP_FT, 12, kFeatWide | kFeatFin>, smem) : go(k_step<STEP_FT, 12, kFeatWide>, smem);
     else if (feat == kFeatStage) go(k_step<STEP_FT, 12, kFeatStage>, ssm);
+    else if (H.tys_bytes && !fin && minb == 12) go(k_step<STEP_FT, 12, kFeatTyS>, H.tys_bytes);
     else if (minb == 12) fin ? go(k_step<STEP_FT, 12, kFeatFin>, smem) : go(k_step<STEP_FT, 12, 0>, smem);
     else fin ? go(k_step<STEP_FT, 8, kFeatFin>, smem) : go(k_step<STEP_FT, 8, 0>, smem);
   }
