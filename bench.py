@@ -14,7 +14,8 @@ outputs inside the timed region).
 
 Default workload (``--config c5a``): BASELINE configs[4], a batch of 4096
 independent QCPs (n=1000, m=1500 = nonneg(500) + 100 x SOC(10), nnz(A) =
-1.5e4 each), sharded over the ranks (strong scaling of a fixed batch).
+1.5e4 each) per rank: weak scaling, N ranks evaluate N independent batches
+with no data-path collective (``--strong`` shards one batch instead).
 ``--config c5b`` at N > 1 splits the ONE LASSO problem by the rows of A
 over the ranks (dist.py; strong scaling; one NCCL sum-allreduce of the A'
 partials per operator step, inside the LSMR graphs).  The other
@@ -56,7 +57,8 @@ def parse():
     ap.add_argument("--config", default="c5a", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lsmr-iters", type=int, default=100)
-    ap.add_argument("--batch", type=int, default=None, help="override the c5a batch size")
+    ap.add_argument("--batch", type=int, default=None, help="override the c5a batch size (per rank)")
+    ap.add_argument("--strong", action="store_true", help="c5a: shard ONE batch over the ranks (strong scaling)")
     ap.add_argument("--cpu-sample", type=int, default=None, help="problems in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -111,15 +113,24 @@ def shard_range(total, rank, world):
     return rank * total // world, (rank + 1) * total // world
 
 
-def build_workload(cfg, rank, world, batch_override=None):
-    """This rank's share of the workload (synthetic, seeded per rank)."""
+def build_workload(cfg, rank, world, batch_override=None, strong=False):
+    """This rank's share of the workload (synthetic, seeded per rank).
+
+    Batches of independent problems (c5a) scale WEAK by default: every rank
+    evaluates its own batch of BATCH[cfg] problems (the per-GPU work of the
+    N=1 line), so N ranks evaluate N times as many problems -- the tier rule
+    for a path that partitions into independent objects.  ``strong`` shards
+    one fixed batch over the ranks instead (``--strong``)."""
     from paper_2508_17522_b200 import synth
 
     if cfg in BATCH:
-        total = batch_override or BATCH[cfg]
-        lo, hi = shard_range(total, rank, world)
-        bt = synth.generate(cfg, seed=1000 + rank, batch=hi - lo)
-        return bt, synth.directions(bt, seed=2000 + rank), total, hi - lo, "strong"
+        per = batch_override or BATCH[cfg]
+        if strong:
+            lo, hi = shard_range(per, rank, world)
+            bt = synth.generate(cfg, seed=1000 + rank, batch=hi - lo)
+            return bt, synth.directions(bt, seed=2000 + rank), per, hi - lo, "strong"
+        bt = synth.generate(cfg, seed=1000 + rank, batch=per)
+        return bt, synth.directions(bt, seed=2000 + rank), per * world, per, "weak"
     if cfg in PARTITIONED and world > 1:
         # one problem, rows of A split over the ranks (SURVEY §8(e)); every
         # rank builds the same instance and keeps its rows
@@ -241,7 +252,7 @@ def run_ours(args):
     from paper_2508_17522_b200 import _native as N
     from paper_2508_17522_b200 import QCPBatch
 
-    bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch)
+    bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch, args.strong)
     K = args.lsmr_iters
     kw = dict(atol=0.0, btol=0.0, max_iter=K)
     blocks = bt.blocks  # (kind, dim, order, alpha) per block; shared list objects convert once
@@ -351,7 +362,10 @@ def run_ours(args):
                        "per_rank_problems": units_here,
                        "lsmr": f"fixed cap K={K} (atol=btol=0) for jvp and vjp; step includes batch preparation",
                        "l2": "256 MiB L2 flush between timed steps (excluded from timing)",
-                       "parallelism": (f"row shards of one problem x{world} (NCCL allreduce of the A' partials)" if comm else f"{'batch shards' if scaling == 'strong' else 'replicas'} x{world}")},
+                       "parallelism": (f"row shards of one problem x{world} (NCCL allreduce of the A' partials)" if comm
+                                       else f"one shard of a fixed batch per rank x{world}" if scaling == "strong"
+                                       else f"an independent batch of {units_here} per rank x{world}"
+                                       if args.config in BATCH else f"replicas x{world}")},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(), "lsmr_iterations_per_s": round(value * 2 * K, 1),
         }

@@ -177,6 +177,7 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   // small problems get small units (all SMs busy, short per-warp chains),
   // large batches amortise per-CTA work over up to 16k entries
   int64_t target_nnz = std::max<int64_t>(256, std::min<int64_t>(16384, total / (8 * 148) + 1));
+  if (const char *e = std::getenv("QG_TARGET_NNZ")) target_nnz = std::max<int64_t>(64, std::atoll(e));  // A/B
   const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
   const int64_t target_rows_y = std::max<int64_t>(8, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
 

@@ -30,8 +30,9 @@ def _worker(rank, world, port, out):
     # each rank owns its shard; timing is max-reduced, counts sum-reduced
     t = bench.max_over_ranks(dist, float(rank + 1))
     n = bench.sum_over_ranks(dist, float(hi - lo))
-    bt, dirs, total, here, scaling = bench.build_workload("c5a", rank, world, batch_override=6)
-    out[rank] = (lo, hi, t, n, total, here, scaling, bt.B, float(bt.x[0]))
+    bt, dirs, total, here, scaling = bench.build_workload("c5a", rank, world, batch_override=6, strong=True)
+    wk = bench.build_workload("c5a", rank, world, batch_override=3)
+    out[rank] = (lo, hi, t, n, total, here, scaling, bt.B, float(bt.x[0]), (wk[2], wk[3], wk[4], wk[0].B))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -41,13 +42,15 @@ def test_sharding_and_reductions_world2():
     port = _free_port()
     out = mp.Manager().dict()
     mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
-    (lo0, hi0, t0, n0, tot0, h0, sc0, b0, x0), (lo1, hi1, t1, n1, tot1, h1, sc1, b1, x1) = out[0], out[1]
+    (lo0, hi0, t0, n0, tot0, h0, sc0, b0, x0, w0), (lo1, hi1, t1, n1, tot1, h1, sc1, b1, x1, w1) = out[0], out[1]
     assert (lo0, hi0, lo1, hi1) == (0, 5, 5, 10)          # disjoint, contiguous, covering
     assert t0 == t1 == 2.0                                  # max over ranks
     assert n0 == n1 == 10.0                                 # every problem counted once
-    assert tot0 == tot1 == 6 and h0 + h1 == 6 and b0 + b1 == 6
+    assert tot0 == tot1 == 6 and h0 + h1 == 6 and b0 + b1 == 6   # --strong: one batch sharded
     assert sc0 == sc1 == "strong"
     assert x0 != x1                                         # ranks build different problems
+    # default (weak): every rank its own batch of 3, 6 evaluated in total
+    assert w0 == w1 == (6, 3, "weak", 3)
 
 
 def test_shard_range_balanced():
