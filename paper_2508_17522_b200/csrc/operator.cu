@@ -799,12 +799,21 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   // QG_STEP_MINB=8|12 overrides.
   static const char *env_minb = std::getenv("QG_STEP_MINB");
   const bool sell = H.nslice_x + H.nslice_y > 0;
-  const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (sell && kind == STEP_F ? 8 : 12);
+  const int minb = env_minb ? std::atoi(env_minb) : (sell && kind == STEP_F ? 8 : 12);
+  static const char *env_carve = std::getenv("QG_CARVEOUT");  // A/B: preferred smem carveout (percent)
   auto go = [&](auto kern, size_t sm_bytes) {
     if (sm_bytes > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
+    if (env_carve)
+      QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env_carve)));
     kern<<<grid, threads, sm_bytes, st>>>(M, a);
   };
+  if (minb == 10 && !a.done && !(H.comm || a.rk1 || H.has_wide || H.stage_bytes)) {  // A/B: 10 CTAs/SM
+    if (kind == STEP_F) go(k_step<STEP_F, 10, 0>, 0);
+    else go(k_step<STEP_FT, 10, 0>, smem);
+    QG_LAUNCHED();
+    return;
+  }
   // the CTA-per-row path and the rarely used features run as their own
   // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
   // partitioned / rank-one steps the all-features one
