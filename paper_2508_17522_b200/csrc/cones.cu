@@ -165,8 +165,8 @@ size_t ConeTable::psd_smem_prep() const {
 }
 
 size_t ConeTable::psd_smem_apply() const {
-  const int d = max_psd_order;
-  return (size_t)4 * d * (d + 1) * sizeof(double);
+  const int dp = (max_psd_order + 3) & ~3;  // psd_pad (dpi_dev.cuh)
+  return (size_t)4 * dp * (dp + 1) * sizeof(double);
 }
 
 void ConeTable::prepare(const double *z, double *proj, int dual_mode, bool want_deriv, cudaStream_t st) {

@@ -47,27 +47,38 @@ __device__ __forceinline__ void soc_apply_warp(const double *zb, int dim, double
   }
 }
 
-// d x d product C = sum_k a(i,k) b(k,j), 2x2 register tiles per thread
-// (halves shared-memory traffic per FMA); out(i, j, c) stores.
-template <class FA, class FB, class FO>
-__device__ __forceinline__ void mm_tiles(int d, FA a, FB b, FO out) {
-  const int nt = (d + 1) / 2;
-  for (int t = threadIdx.x; t < nt * nt; t += blockDim.x) {
-    const int i0 = 2 * (t % nt), j0 = 2 * (t / nt);
-    const bool i1 = i0 + 1 < d, j1 = j0 + 1 < d;
-    double c00 = 0.0, c01 = 0.0, c10 = 0.0, c11 = 0.0;
+// d x d product C = sum_k a(i,k) b(k,j) with TI x TJ register tiles per
+// thread (TI + TJ shared-memory loads per TI*TJ FMAs); out(i, j, c) stores.
+// lower = true: only tiles touching the lower triangle (j <= i) are computed
+// (symmetric results / lower-triangle consumers).  a/b must return 0 for
+// indices >= d (the padded operand matrices are zero-filled).
+template <int TI, int TJ, class FA, class FB, class FO>
+__device__ __forceinline__ void mm_tiles(int d, bool lower, FA a, FB b, FO out) {
+  const int ni = (d + TI - 1) / TI, nj = (d + TJ - 1) / TJ;
+  for (int t = threadIdx.x; t < ni * nj; t += blockDim.x) {
+    const int i0 = TI * (t % ni), j0 = TJ * (t / ni);
+    if (lower && j0 > i0 + TI - 1) continue;
+    double c[TI][TJ];
+#pragma unroll
+    for (int x = 0; x < TI; ++x)
+#pragma unroll
+      for (int y = 0; y < TJ; ++y) c[x][y] = 0.0;
     for (int k = 0; k < d; ++k) {
-      const double a0 = a(i0, k), a1 = i1 ? a(i0 + 1, k) : 0.0;
-      const double b0 = b(k, j0), b1 = j1 ? b(k, j0 + 1) : 0.0;
-      c00 += a0 * b0;
-      c10 += a1 * b0;
-      c01 += a0 * b1;
-      c11 += a1 * b1;
+      double av[TI], bv[TJ];
+#pragma unroll
+      for (int x = 0; x < TI; ++x) av[x] = a(i0 + x, k);
+#pragma unroll
+      for (int y = 0; y < TJ; ++y) bv[y] = b(k, j0 + y);
+#pragma unroll
+      for (int x = 0; x < TI; ++x)
+#pragma unroll
+        for (int y = 0; y < TJ; ++y) c[x][y] += av[x] * bv[y];
     }
-    out(i0, j0, c00);
-    if (i1) out(i0 + 1, j0, c10);
-    if (j1) out(i0, j0 + 1, c01);
-    if (i1 && j1) out(i0 + 1, j0 + 1, c11);
+#pragma unroll
+    for (int x = 0; x < TI; ++x)
+#pragma unroll
+      for (int y = 0; y < TJ; ++y)
+        if (i0 + x < d && j0 + y < d) out(i0 + x, j0 + y, c[x][y]);
   }
 }
 
@@ -75,35 +86,54 @@ __device__ __forceinline__ void mm_tiles(int d, FA a, FB b, FO out) {
 // evaluated as V' (S V).  CTA-wide; smem holds 4 padded (d x (d+1))
 // matrices (leading dimension d+1 breaks the column-stride bank conflicts).
 // V, B column-major (d x d) in global.
+// Matrices are padded to dp = d rounded up to 4 (zero rows / columns) so the
+// 4x2 register tiles never leave the arrays; V'T V and the final product are
+// symmetric, so only their lower triangles are computed (3 d^3 instead of
+// 4 d^3 FMAs; c4: 512 blocks of order 32 per F' step).
+static __device__ __forceinline__ int psd_pad(int d) { return (d + 3) & ~3; }
+
 static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
                                      double *sm) {
-  const int ld = d + 1, sz = d * ld;
+  const int dp = psd_pad(d), ld = dp + 1, sz = dp * ld;
   double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = sm + 3 * sz;
-  for (int idx = threadIdx.x; idx < d * d; idx += blockDim.x) {
-    const int i = idx % d, j = idx / d;
-    V[i + j * ld] = Vg[idx];
-    const int a = i >= j ? i : j, b = i >= j ? j : i;
-    const double v = in[svec_index(a, b, d)];
-    S[i + j * ld] = (a == b) ? v : v / kSqrt2;
+  for (int idx = threadIdx.x; idx < dp * dp; idx += blockDim.x) {
+    const int i = idx % dp, j = idx / dp;
+    const bool in_d = i < d && j < d;
+    V[i + j * ld] = in_d ? Vg[i + j * d] : 0.0;
+    double s = 0.0;
+    if (in_d) {
+      const int a = i >= j ? i : j, b = i >= j ? j : i;
+      const double v = in[svec_index(a, b, d)];
+      s = (a == b) ? v : v / kSqrt2;
+    }
+    S[i + j * ld] = s;
+    T[i + j * ld] = 0.0;
+    W[i + j * ld] = 0.0;
   }
   __syncthreads();
   // T = S V
-  mm_tiles(d, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
-           [&](int i, int j, double c) { T[i + j * ld] = c; });
+  mm_tiles<4, 2>(d, false, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
+                 [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
-  // W = (V' T) o B
-  mm_tiles(d, [&](int i, int k) { return V[k + i * ld]; }, [&](int k, int j) { return T[k + j * ld]; },
-           [&](int i, int j, double c) { W[i + j * ld] = Bg[i + j * d] * c; });
+  // W = (V' T) o B, symmetric: lower triangle computed, mirrored
+  mm_tiles<4, 2>(d, true, [&](int i, int k) { return V[k + i * ld]; }, [&](int k, int j) { return T[k + j * ld]; },
+                 [&](int i, int j, double c) {
+                   if (i >= j) {
+                     const double w = Bg[i + j * d] * c;
+                     W[i + j * ld] = w;
+                     W[j + i * ld] = w;
+                   }
+                 });
   __syncthreads();
   // T = V W
-  mm_tiles(d, [&](int i, int k) { return V[i + k * ld]; }, [&](int k, int j) { return W[k + j * ld]; },
-           [&](int i, int j, double c) { T[i + j * ld] = c; });
+  mm_tiles<4, 2>(d, false, [&](int i, int k) { return V[i + k * ld]; }, [&](int k, int j) { return W[k + j * ld]; },
+                 [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
   // out = svec(T V') on the lower triangle
-  mm_tiles(d, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
-           [&](int i, int j, double c) {
-             if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
-           });
+  mm_tiles<4, 2>(d, true, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
+                 [&](int i, int j, double c) {
+                   if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
+                 });
   __syncthreads();
 }
 
