@@ -192,8 +192,9 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
   const bool isx = ui < M.nxu;
-  const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];
+  const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];  // preparation-time data: before the PDL wait
   const int p = u.prob;
+  pdl_wait();  // the previous kernel's vectors / LSMR state are complete past this point
   double s_in, c_out;
   if (!lsmr_runs(a, p, s_in, c_out)) {  // CTA-uniform
     // a skipped v-step (beta = 0) still runs its finalize recurrences
@@ -353,6 +354,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
       }
     }
   }
+  pdl_trigger();  // the next kernel may start launching (it waits for our completion)
   double tot[kSlots];
   cta_sum_slots(acc, red, tot);
   if (threadIdx.x == 0 && a.part)
@@ -681,6 +683,8 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
 }
 
 __global__ void k_fin(Mats M, FinArgs a) {
+  pdl_wait();
+  pdl_trigger();
   const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (p < a.B) fin_problem(M, a, p, threadIdx.x & 31);
 }
@@ -765,6 +769,26 @@ Mats make_mats(const Handle &H) {
 
 static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
 
+// Launch with programmatic stream serialization (see pdl_wait / pdl_trigger
+// in qg_common.cuh); QG_PDL=0 falls back to ordinary serialization (A/B).
+template <class... KArgs, class... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args &&...args) {
+  static const char *env = std::getenv("QG_PDL");
+  static const bool pdl = !env || std::atoi(env) != 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  QG_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
+
 static void launch_step_one(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
 
 // One operator step.  Row-partitioned handles split it around the exchange:
@@ -806,7 +830,7 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
     if (env_carve)
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env_carve)));
-    kern<<<grid, threads, sm_bytes, st>>>(M, a);
+    launch_pdl(kern, dim3(grid), dim3(threads), sm_bytes, st, M, a);
   };
   if (minb == 10 && !a.done && !(H.comm || a.rk1 || H.has_wide || H.stage_bytes)) {  // A/B: 10 CTAs/SM
     if (kind == STEP_F) go(k_step<STEP_F, 10, 0>, 0);
@@ -862,7 +886,7 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
     a.py = H.psum + (size_t)H.B * kSlots;
     a.px_ptr = a.py_ptr = H.d_iota;
   }
-  k_fin<<<grid, 256, 0, st>>>(M, a);
+  launch_pdl(k_fin, dim3(grid), dim3(256), 0, st, M, a);
   QG_LAUNCHED();
 }
 

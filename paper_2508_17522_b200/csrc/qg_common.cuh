@@ -134,6 +134,15 @@ void host_parallel(int64_t n, int64_t min_chunk, F fn) {
 void *pinned_staging(size_t bytes, int slot);
 
 // ---------------------------------------------------------- device utils --
+// Programmatic dependent launch (sm_90+): the LSMR loop's kernels are
+// launched with programmatic stream serialization, so the next kernel's
+// launch and CTA scheduling overlap this one's tail.  Every such kernel
+// waits (pdl_wait) before its first read of data produced by the previous
+// kernel, and lets the next one start (pdl_trigger) once its main work is
+// issued.  Both are no-ops for ordinary launches.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
