@@ -174,7 +174,8 @@ constexpr int kStepThreads = 128;
 constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16, kFeatTyS = 32;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
-__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane);
+__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
+                                            const double *pre = nullptr);
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
@@ -492,24 +493,37 @@ __global__ void k_part_reduce(const double *px, const int64_t *px_ptr, const dou
 }
 
 // Finalize of problem p by one warp (all 32 lanes call it).
-__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane) {
+__device__ __forceinline__ bool fin_skips(const FinArgs &a, int p) {
+  // inactive problems have nothing to finalize (a skipped v-step still runs
+  // its recurrences: skip_v problems stay active)
+  return a.st && a.phase != PH_APPLY && a.phase != PH_RHS && !a.st[p].active;
+}
+
+// pre: the 2 x kSlots per-problem sums already reduced (CTA-per-problem
+// finalize); else the warp reduces them (all 32 lanes call).
+__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
+                                            const double *pre) {
   // partials are read L2-coherent (__ldcg): in the fused variant they were
   // written by other CTAs of the same launch
   Lsmr *L = a.st ? a.st + p : nullptr;
-  if (L && a.phase != PH_APPLY && a.phase != PH_RHS && !L->active) return;
-  if (L && a.phase == PH_STEP_V && L->skip_v) {
-    // fall through: v-step did not run, only the recurrences do
-  }
+  if (fin_skips(a, p)) return;
   // deterministic per-problem sums of the producers' partials (fixed order)
   double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
-  for (int64_t k = a.px_ptr[p] + lane; k < a.px_ptr[p + 1]; k += 32)
+  if (pre) {
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sx[j] += __ldcg(a.px + k * kSlots + j);
-  for (int64_t k = a.py_ptr[p] + lane; k < a.py_ptr[p + 1]; k += 32)
+    for (int j = 0; j < kSlots; ++j) { sx[j] = pre[j]; sy[j] = pre[kSlots + j]; }
+  } else {
+#pragma unroll 4
+    for (int64_t k = a.px_ptr[p] + lane; k < a.px_ptr[p + 1]; k += 32)
 #pragma unroll
-    for (int j = 0; j < kSlots; ++j) sy[j] += __ldcg(a.py + k * kSlots + j);
+      for (int j = 0; j < kSlots; ++j) sx[j] += __ldcg(a.px + k * kSlots + j);
+#pragma unroll 4
+    for (int64_t k = a.py_ptr[p] + lane; k < a.py_ptr[p + 1]; k += 32)
 #pragma unroll
-  for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
+      for (int j = 0; j < kSlots; ++j) sy[j] += __ldcg(a.py + k * kSlots + j);
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
+  }
   if (lane != 0) return;
   const Embed E = M.emb[p];
   const int64_t T = M.NX + M.NY + p;
@@ -687,6 +701,45 @@ __global__ void k_fin(Mats M, FinArgs a) {
   pdl_trigger();
   const int p = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (p < a.B) fin_problem(M, a, p, threadIdx.x & 31);
+}
+
+// CTA per problem, for batches whose problems have many work units (small
+// single problems cut into hundreds of units): 256 threads stride over the
+// slots, fixed-order CTA reduction, thread 0 runs the scalar part.  The
+// warp-per-problem version spent ~25 sequential L2 round trips per lane
+// summing c2's ~800 slots.
+__global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  const int p = (int)blockIdx.x;
+  if (fin_skips(a, p)) return;  // CTA-uniform
+  __shared__ double red[(256 / 32) * 2 * kSlots];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  double s[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 2
+  for (int64_t k = a.px_ptr[p] + threadIdx.x; k < a.px_ptr[p + 1]; k += blockDim.x)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) s[j] += __ldcg(a.px + k * kSlots + j);
+#pragma unroll 2
+  for (int64_t k = a.py_ptr[p] + threadIdx.x; k < a.py_ptr[p + 1]; k += blockDim.x)
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) s[kSlots + j] += __ldcg(a.py + k * kSlots + j);
+#pragma unroll
+  for (int j = 0; j < 2 * kSlots; ++j) s[j] = warp_sum(s[j]);
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < 2 * kSlots; ++j) red[warp * 2 * kSlots + j] = s[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double pre[2 * kSlots];
+#pragma unroll
+    for (int j = 0; j < 2 * kSlots; ++j) {
+      double t = red[j];
+      for (int w = 1; w < nw; ++w) t += red[w * 2 * kSlots + j];
+      pre[j] = t;
+    }
+    fin_problem(M, a, p, 0, pre);
+  }
 }
 
 // Persistent LSMR for small batches (launch latency, not bandwidth, bounds
@@ -886,7 +939,12 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
     a.py = H.psum + (size_t)H.B * kSlots;
     a.px_ptr = a.py_ptr = H.d_iota;
   }
-  launch_pdl(k_fin, dim3(grid), dim3(256), 0, st, M, a);
+  // many work units per problem (>= 64 on average): a CTA per problem.
+  // QG_FIN_CTA=0|1 forces (A/B).
+  static const char *env = std::getenv("QG_FIN_CTA");
+  const bool cta = !H.comm && (env ? std::atoi(env) != 0 : (int64_t)(H.nxu() + H.nyu()) >= 64LL * H.B);
+  if (cta) launch_pdl(k_fin_cta, dim3((unsigned)H.B), dim3(256), 0, st, M, a);
+  else launch_pdl(k_fin, dim3(grid), dim3(256), 0, st, M, a);
   QG_LAUNCHED();
 }
 
