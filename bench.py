@@ -413,8 +413,9 @@ def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=N
     sample is about ``target_s`` seconds of CPU work."""
     if args.cpu_sample:
         return args.cpu_sample
-    base = cores if scaling == "strong" else 1
-    if target_s is None or bt is None or scaling != "strong":
+    batched = args.config in BATCH   # many independent problems: one per host core
+    base = cores if batched else 1
+    if target_s is None or bt is None or not batched:
         return base
     from oracle import cpu_bench
 

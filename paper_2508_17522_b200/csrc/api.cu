@@ -320,7 +320,7 @@ static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &
 static bool fused_fin_ok(const Handle &H) {
   static const char *env = std::getenv("QG_FUSED_FIN");
   if (!env || !std::atoi(env)) return false;
-  return !H.comm && !H.use_rk1 && !H.stage_bytes;
+  return !H.comm && !H.use_rk1;
 }
 
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {

@@ -82,8 +82,6 @@ struct Handle {
   int32_t *y_rowof = nullptr;
   int64_t nslice_x = 0, nslice_y = 0;
   bool has_wide = false;        // some unit runs CTA-per-row (MODE_WIDE)
-  size_t stage_bytes = 0;       // > 0: step kernels stage each problem's vectors in smem
-  size_t tys_bytes = 0;         // > 0: the F' step keeps the Y-side t = g - w in smem
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;

@@ -46,8 +46,7 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
                                          const double *v2, const double *x1, const double *x2, int G,
-                                         int64_t b1, int64_t b2, const double *vs1, const double *vs2,
-                                         RowFn row) {
+                                         int64_t b1, int64_t b2, RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
     // warps claim pairs of slices dynamically (balances uneven units)
@@ -63,13 +62,8 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
       double a1, b1v, a2 = 0.0, b2v = 0.0;
-      // vs1 / vs2: the problem's input vectors staged in shared memory
-      if (vs1) sell_dot2_local(S1, s, sb, lane, vs1, (int)b1, a1, b1v);
-      else sell_dot2<UNR>(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
-      if (S2) {
-        if (vs2) sell_dot2_local(*S2, s, sb, lane, vs2, (int)b2, a2, b2v);
-        else sell_dot2<UNR>(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
-      }
+      sell_dot2<UNR>(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
+      if (S2) sell_dot2<UNR>(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
     }
@@ -171,7 +165,7 @@ constexpr int kStepThreads = 128;
 #ifndef QG_FT_UNROLL
 #define QG_FT_UNROLL 2
 #endif
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatStage = 8, kFeatFin = 16, kFeatTyS = 32;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatFin = 16;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
@@ -179,15 +173,14 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
-// a.rk1 is set), kFeatStage (smem-staged gathers), kFeatFin (fused finalize).
+// a.rk1 is set), kFeatFin (fused finalize).
 // The common variant (0) carries none of them.
 // One work unit (`ui`: X units then Y units) of an operator step, by the
 // whole CTA; the partial-sum slot of the unit is part[ui].
 template <int KIND, int FEAT>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
-  constexpr bool kStage = (FEAT & kFeatStage) != 0, kFin = (FEAT & kFeatFin) != 0;
-  constexpr bool kTyS = (FEAT & kFeatTyS) != 0;
+  constexpr bool kFin = (FEAT & kFeatFin) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
@@ -227,28 +220,12 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     }
   }
 
-  // kStage: the problem's input vectors go to shared memory once per CTA, so
-  // every SELL gather is an LDS instead of an L1/L2 round trip
-  const double *vx = nullptr, *vy = nullptr;
-  if (kStage && u.mode == MODE_SELL) {  // CTA-uniform
-    const int64_t xo = M.xoff[p], nx = M.xoff[p + 1] - xo;
-    for (int64_t i = threadIdx.x; i < nx; i += blockDim.x) sm[i] = inX[xo + i];
-    vx = sm;
-    if (isx) {
-      const double *y2 = KIND == STEP_F ? a.dpin : inY;
-      const int64_t yo = M.yoff[p], ny = M.yoff[p + 1] - yo;
-      for (int64_t i = threadIdx.x; i < ny; i += blockDim.x) sm[nx + i] = y2[yo + i];
-      vy = sm + nx;
-    }
-    __syncthreads();
-  }
-
   if (isx) {
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
       for_rows<kWide, kUnr>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
-               u.lanes, M.yoff[p], 0, nullptr, nullptr, [&](int r, double s, double) { a.xred[r] = s; });
+               u.lanes, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
     auto xrow = [&](int r, double s1, double s2) {
@@ -273,10 +250,10 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
              };
     if (kDist && a.xmode == X_FINISH)
       for_rows<kWide, kUnr>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0, nullptr, nullptr, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
+               M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
       for_rows<kWide, kUnr>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
-               M.xoff[p], M.yoff[p], vx, vy, xrow);
+               M.xoff[p], M.yoff[p], xrow);
     if (kDist && !M.x_owner)
 #pragma unroll
       for (int k = 0; k < kSlots; ++k) acc[k] = 0.0;  // replicated rows: rank 0 counts them
@@ -285,7 +262,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
       for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0, vx, nullptr,
+               M.xoff[p], 0,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
                  const double o2 = (-s) + wN * M.b[r];
@@ -297,13 +274,10 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                  acc[2] += o * o;
                });
     } else {
-      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit; kTyS keeps
-      // t in shared memory (rows [row0, row1) at sm[0..)) instead of an HBM
-      // round trip -- handles whose Y units all take the register / thread-
-      // per-block epilogues (no PSD, SOC dims <= 32)
-      double *tY = kTyS ? (sm - u.row0) : a.tY;
+      // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
+      double *tY = a.tY;
       for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
-               M.xoff[p], 0, vx, nullptr,
+               M.xoff[p], 0,
                [&](int r, double s, double) {
                  tY[r] = (s - wN * M.b[r]) - inY[r];
                  if (kRk1) acc[3] += a.rk1[M.NX + r] * inY[r];
@@ -873,44 +847,30 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   // (64 registers, 8 CTAs/SM measured best: c5a 0.460 vs 0.509 ms); the F'
   // step (two-pass Y side, epilogue) and the CSR group path gain from 12
   // CTAs/SM (c5a F' 0.625 -> 0.574 ms; c3: 11.2 -> 8.7 ms per jvp).
-  // QG_STEP_MINB=8|12 overrides.
+  // QG_STEP_MINB=8|12 overrides (10 CTAs/SM, 48 registers, measured slower for
+  // both steps).
   static const char *env_minb = std::getenv("QG_STEP_MINB");
   const bool sell = H.nslice_x + H.nslice_y > 0;
-  const int minb = env_minb ? std::atoi(env_minb) : (sell && kind == STEP_F ? 8 : 12);
-  static const char *env_carve = std::getenv("QG_CARVEOUT");  // A/B: preferred smem carveout (percent)
+  const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (sell && kind == STEP_F ? 8 : 12);
   auto go = [&](auto kern, size_t sm_bytes) {
     if (sm_bytes > 48 * 1024)
       QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
-    if (env_carve)
-      QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env_carve)));
     launch_pdl(kern, dim3(grid), dim3(threads), sm_bytes, st, M, a);
   };
-  if (minb == 10 && !a.done && !(H.comm || a.rk1 || H.has_wide || H.stage_bytes)) {  // A/B: 10 CTAs/SM
-    if (kind == STEP_F) go(k_step<STEP_F, 10, 0>, 0);
-    else go(k_step<STEP_FT, 10, 0>, smem);
-    QG_LAUNCHED();
-    return;
-  }
   // the CTA-per-row path and the rarely used features run as their own
   // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
-  // partitioned / rank-one steps the all-features one
-  // Staged variant: SELL handles whose problems' vectors fit (H.stage_bytes)
-  // Fused finalize (a.done set by the loop driver: whole-problem handles, no
-  // rank-one term, no staging): its own plain / wide variants.
-  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : (H.stage_bytes ? kFeatStage : 0));
-  const size_t ssm = std::max(smem, H.stage_bytes);
-  const bool fin = a.done != nullptr && (feat == 0 || feat == kFeatWide);
+  // partitioned / rank-one steps the all-features one.  The fused finalize
+  // (a.done set by the loop driver) has its own plain / wide variants.
+  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
+  const bool fin = a.done != nullptr && feat != kFeatAll;
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
     else if (feat == kFeatWide) fin ? go(k_step<STEP_F, 12, kFeatWide | kFeatFin>, 0) : go(k_step<STEP_F, 12, kFeatWide>, 0);
-    else if (feat == kFeatStage) go(k_step<STEP_F, 8, kFeatStage>, ssm);
     else if (minb == 12) fin ? go(k_step<STEP_F, 12, kFeatFin>, 0) : go(k_step<STEP_F, 12, 0>, 0);
     else fin ? go(k_step<STEP_F, 8, kFeatFin>, 0) : go(k_step<STEP_F, 8, 0>, 0);
   } else {
     if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
     else if (feat == kFeatWide) fin ? go(k_step<STEP_FT, 12, kFeatWide | kFeatFin>, smem) : go(k_step<STEP_FT, 12, kFeatWide>, smem);
-    else if (feat == kFeatStage) go(k_step<STEP_FT, 12, kFeatStage>, ssm);
-    else if (H.tys_bytes && !fin && minb == 12) go(k_step<STEP_FT, 12, kFeatTyS>, H.tys_bytes);
     else if (minb == 12) fin ? go(k_step<STEP_FT, 12, kFeatFin>, smem) : go(k_step<STEP_FT, 12, 0>, smem);
     else fin ? go(k_step<STEP_FT, 8, kFeatFin>, smem) : go(k_step<STEP_FT, 8, 0>, smem);
   }
@@ -956,7 +916,7 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
 // launches, and four grid barriers per iteration cost more than four graph
 // kernel nodes.
 bool persistent_ok(const Handle &H) {
-  if (H.comm || H.use_rk1 || H.has_wide || H.stage_bytes) return false;
+  if (H.comm || H.use_rk1 || H.has_wide) return false;
   static const char *env = std::getenv("QG_PERSIST");
   return env && std::atoi(env) != 0;
 }

@@ -128,47 +128,6 @@ __device__ __forceinline__ double row_dot32(const int32_t *rp, const int32_t *co
   return s;
 }
 
-// sell_dot2 against a problem vector staged in shared memory (vs = the
-// problem's slice, base = its first global index): index = local column.
-template <class Idx>
-__device__ __forceinline__ void sell_dot2_local_t(const SellView &S, const Idx *colp, int64_t sa, int64_t sb,
-                                                  int lane, const double *vs, int base, double &acc_a,
-                                                  double &acc_b) {
-  const int64_t oa = S.off[sa] + lane;
-  const int wa = S.w[sa];
-  const int64_t ob = sb >= 0 ? S.off[sb] + lane : 0;
-  const int wb = sb >= 0 ? S.w[sb] : 0;
-  const int wm = wa < wb ? wa : wb;
-  double a = 0.0, b = 0.0;
-  int k = 0;
-#pragma unroll 4
-  for (; k < wm; ++k) {
-    const int64_t pa = oa + 32LL * k, pb = ob + 32LL * k;
-    const double va = ld_stream(S.val + pa), vb = ld_stream(S.val + pb);
-    const int ca = (int)ld_stream(colp + pa) - base, cb = (int)ld_stream(colp + pb) - base;
-    a += va * vs[ca];
-    b += vb * vs[cb];
-  }
-#pragma unroll 4
-  for (int j = k; j < wa; ++j) {
-    const int64_t pa = oa + 32LL * j;
-    a += ld_stream(S.val + pa) * vs[(int)ld_stream(colp + pa) - base];
-  }
-#pragma unroll 4
-  for (int j = k; j < wb; ++j) {
-    const int64_t pb = ob + 32LL * j;
-    b += ld_stream(S.val + pb) * vs[(int)ld_stream(colp + pb) - base];
-  }
-  acc_a = a;
-  acc_b = b;
-}
-
-__device__ __forceinline__ void sell_dot2_local(const SellView &S, int64_t sa, int64_t sb, int lane,
-                                                const double *vs, int base, double &acc_a, double &acc_b) {
-  if (S.col16) sell_dot2_local_t(S, S.col16, sa, sb, lane, vs, 0, acc_a, acc_b);
-  else sell_dot2_local_t(S, S.col, sa, sb, lane, vs, base, acc_a, acc_b);
-}
-
 // Group-of-G sum inside a warp (G power of two, runtime).
 __device__ __forceinline__ double gsum(double v, int G) {
   for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -263,33 +263,9 @@ void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_
   H.has_wide = false;
   for (const auto *us : {&H.xunits, &H.cones.units})
     for (const Unit &u : *us) H.has_wide = H.has_wide || u.mode == MODE_WIDE;
-  // F' Y side: t = g - w kept in shared memory when every Y unit takes the
-  // register (elementwise), thread-per-block (3-cones, SOC dims <= 32)
-  // epilogue and its rows fit 32 KB.  Opt-in (QG_TYS=1): measured neutral to
-  // slightly slower (c5a F' 0.527 -> 0.534 ms; c2, c3 unchanged).
-  H.tys_bytes = 0;
-  const char *tys = std::getenv("QG_TYS");
-  if (tys && std::atoi(tys) && H.cones.max_psd_order == 0) {
-    int64_t rows = 0;
-    bool ok = true;
-    for (const Unit &u : H.cones.units) {
-      ok = ok && u.cls != CLS_PSD && (u.cls != CLS_SOC || u.group > 0);
-      rows = std::max<int64_t>(rows, u.row1 - u.row0);
-    }
-    if (ok && rows > 0 && rows * 8 <= 32 * 1024) H.tys_bytes = (size_t)rows * 8;
-  }
-  // Shared-memory staging of the per-problem vectors for SELL gathers (when
-  // the largest problem's X + Y vectors fit 24 KB and no PSD block needs the
-  // dynamic smem): opt-in with QG_STAGE=1.  Measured on c5a it LOSES (F 0.457
-  // -> 0.494 ms, F' 0.58 -> 0.88 ms: fewer resident CTAs, LDS bank conflicts,
-  // the staging pass itself) -- L1 already serves most gathers.
-  H.stage_bytes = 0;
-  const char *stage = std::getenv("QG_STAGE");
-  if ((H.nslice_x + H.nslice_y) > 0 && !H.has_wide && H.cones.max_psd_order == 0 && stage && std::atoi(stage)) {
-    int64_t mx = 0;
-    for (int p = 0; p < H.B; ++p) mx = std::max<int64_t>(mx, H.n[p] + H.m[p]);
-    if (mx * 8 <= 24 * 1024) H.stage_bytes = (size_t)std::max<int64_t>(mx, 1) * 8;
-  }
+  // Measured and removed: shared-memory staging of each
+  // problem's gathered vectors (c5a F 0.457 -> 0.494 ms, F' 0.58 -> 0.88 ms)
+  // and a shared-memory t for the F' Y side (neutral).
 }
 
 }  // namespace qg
