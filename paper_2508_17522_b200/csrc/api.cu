@@ -434,6 +434,15 @@ static int kernels_per_iter(const Handle &H) {
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
   Workspace &W = H.ws;
+  if (resident_ok(H)) {
+    // one launch: each CTA runs whole problems to their stopping rule (the
+    // per-problem caps live in the LSMR state), no host polling
+    StepArgs su, sv;
+    FinArgs fu, fv;
+    iter_args(H, jvp, su, sv, fu, fv);
+    launch_lsmr_resident(H, M, jvp ? STEP_F : STEP_FT, su, sv, fu, fv, st);
+    return;
+  }
   long long done = 0;
   const bool persistent = persistent_ok(H);
   while (true) {

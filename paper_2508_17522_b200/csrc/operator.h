@@ -69,6 +69,11 @@ void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_
 // Persistent cooperative LSMR loop (small batches): eligibility, and one
 // launch running `iters` iterations with the given step / finalize arguments.
 bool persistent_ok(const Handle &H);
+// Problem-resident loop (one CTA runs a whole problem's iterations; batches
+// of many small problems): eligibility and the single launch.
+bool resident_ok(const Handle &H);
+void launch_lsmr_resident(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
+                          const FinArgs &fu, const FinArgs &fv, cudaStream_t st);
 void launch_lsmr_persistent(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
                             const FinArgs &fu, const FinArgs &fv, int iters, cudaStream_t st);
 void launch_count_active(const Handle &H, cudaStream_t st);
