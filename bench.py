@@ -31,7 +31,6 @@ import os
 import statistics
 import subprocess
 import sys
-import time
 
 import numpy as np
 

@@ -10,8 +10,6 @@ exactly the work the GPU arm does per problem (reference solution_map.py:
 import os
 import time
 
-import numpy as np
-
 os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
 os.environ.setdefault("OMP_NUM_THREADS", "1")
 
@@ -49,6 +47,12 @@ _G = {}
 
 def _init(batch, dirs, K):
     _G.update(batch=batch, dirs=dirs, K=K)
+    try:  # one BLAS thread per worker process (numpy may be loaded before the env vars)
+        from threadpoolctl import threadpool_limits
+
+        _G["limits"] = threadpool_limits(1)
+    except ImportError:
+        pass
 
 
 def _work(p):

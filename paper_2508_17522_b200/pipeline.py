@@ -20,7 +20,6 @@ the whole-batch path for ``e2e``.
 
 import numpy as np
 
-from paper_2508_17522_b200 import _native as N
 from paper_2508_17522_b200.solution_map import QCPBatch
 
 _DATA = ("P_colptr", "P_rowidx", "P_vals", "A_colptr", "A_rowidx", "A_vals", "q", "b", "x", "y", "s")

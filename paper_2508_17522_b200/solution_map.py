@@ -25,7 +25,7 @@ from paper_2508_17522_b200 import _native as N
 from paper_2508_17522_b200 import cones
 from paper_2508_17522_b200.embedding import DataPerturbation, ProblemData
 from paper_2508_17522_b200.errors import DomainError, ValidationError
-from paper_2508_17522_b200.sparse import CscMatrix, same_pattern
+from paper_2508_17522_b200.sparse import same_pattern
 
 
 def _vector(name, v, length=None):
