@@ -45,6 +45,19 @@ def eval_one(th, sol, pert, de, K):
 _G = {}
 
 
+def _one_thread():
+    """Context limiting BLAS / OpenMP pools to one thread (numpy may have been
+    imported before the environment variables above took effect)."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        return threadpool_limits(1)
+    except ImportError:
+        import contextlib
+
+        return contextlib.nullcontext()
+
+
 def _init(batch, dirs, K):
     _G.update(batch=batch, dirs=dirs, K=K)
     try:  # one BLAS thread per worker process (numpy may be loaded before the env vars)
@@ -63,10 +76,11 @@ def _work(p):
 def time_sample(batch, dirs, K, problems, workers):
     """Wall seconds to run jvp+vjp on ``problems`` over ``workers`` processes."""
     if workers <= 1:
-        t = time.perf_counter()
-        for p in problems:
-            eval_one(*problem(batch, dirs, p), K)
-        return time.perf_counter() - t
+        with _one_thread():
+            t = time.perf_counter()
+            for p in problems:
+                eval_one(*problem(batch, dirs, p), K)
+            return time.perf_counter() - t
     import multiprocessing as mp
 
     ctx = mp.get_context("fork")
@@ -80,14 +94,16 @@ def time_sample(batch, dirs, K, problems, workers):
 def extrapolated_eval_seconds(batch, dirs, p, K, k_small):
     """Seconds of one jvp+vjp at cap K for problem p, estimated from runs at
     caps 0 (setup only) and k_small: t(K) = t0 + K (t_k - t0) / k_small.
-    Used for configurations whose full-K CPU eval takes minutes."""
+    Used for configurations whose full-K CPU eval takes minutes.  One BLAS
+    thread (the reported ``cores`` is 1)."""
     prob = problem(batch, dirs, p)
-    t = time.perf_counter()
-    eval_one(*prob, 0)
-    t0 = time.perf_counter() - t
-    t = time.perf_counter()
-    eval_one(*prob, k_small)
-    tk = time.perf_counter() - t
+    with _one_thread():
+        t = time.perf_counter()
+        eval_one(*prob, 0)
+        t0 = time.perf_counter() - t
+        t = time.perf_counter()
+        eval_one(*prob, k_small)
+        tk = time.perf_counter() - t
     per_iter = max(tk - t0, 0.0) / k_small
     return t0 + K * per_iter, t0, per_iter
 
