@@ -91,6 +91,14 @@ __device__ __forceinline__ void mm_tiles(int d, bool lower, FA a, FB b, FO out) 
 // symmetric, so only their lower triangles are computed (3 d^3 instead of
 // 4 d^3 FMAs; c4: 512 blocks of order 32 per F' step).
 static __device__ __forceinline__ int psd_pad(int d) { return (d + 3) & ~3; }
+// Register tile of the PSD products.  c4 F' (512 PSD(32) blocks): 2x2 0.137
+// ms, 4x2 0.145 ms, 4x4 0.325 ms (the F' step runs at 40 registers).
+#ifndef PSD_TI
+#define PSD_TI 2
+#endif
+#ifndef PSD_TJ
+#define PSD_TJ 2
+#endif
 
 static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
                                      double *sm) {
@@ -112,11 +120,11 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
   }
   __syncthreads();
   // T = S V
-  mm_tiles<4, 2>(d, false, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
+  mm_tiles<PSD_TI, PSD_TJ>(d, false, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
                  [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
   // W = (V' T) o B, symmetric: lower triangle computed, mirrored
-  mm_tiles<4, 2>(d, true, [&](int i, int k) { return V[k + i * ld]; }, [&](int k, int j) { return T[k + j * ld]; },
+  mm_tiles<PSD_TI, PSD_TJ>(d, true, [&](int i, int k) { return V[k + i * ld]; }, [&](int k, int j) { return T[k + j * ld]; },
                  [&](int i, int j, double c) {
                    if (i >= j) {
                      const double w = Bg[i + j * d] * c;
@@ -126,11 +134,11 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
                  });
   __syncthreads();
   // T = V W
-  mm_tiles<4, 2>(d, false, [&](int i, int k) { return V[i + k * ld]; }, [&](int k, int j) { return W[k + j * ld]; },
+  mm_tiles<PSD_TI, PSD_TJ>(d, false, [&](int i, int k) { return V[i + k * ld]; }, [&](int k, int j) { return W[k + j * ld]; },
                  [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
   // out = svec(T V') on the lower triangle
-  mm_tiles<4, 2>(d, true, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
+  mm_tiles<PSD_TI, PSD_TJ>(d, true, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
                  [&](int i, int j, double c) {
                    if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
                  });
