@@ -87,7 +87,7 @@ __device__ __forceinline__ void mm_tiles(int d, bool lower, FA a, FB b, FO out) 
 // matrices (leading dimension d+1 breaks the column-stride bank conflicts).
 // V, B column-major (d x d) in global.
 // Matrices are padded to dp = d rounded up to 4 (zero rows / columns) so the
-// 4x2 register tiles never leave the arrays; V'T V and the final product are
+// register tiles (up to 4 wide) never leave the arrays; V'T V and the final product are
 // symmetric, so only their lower triangles are computed (3 d^3 instead of
 // 4 d^3 FMAs; c4: 512 blocks of order 32 per F' step).
 static __device__ __forceinline__ int psd_pad(int d) { return (d + 3) & ~3; }
