@@ -764,7 +764,7 @@ __global__ void __launch_bounds__(kStepThreads, 4) k_lsmr_loop(Mats M, LoopArgs 
 // the SM's L1 for the whole solve, and a converged problem frees its CTA at
 // once.  `next` is the claim counter (zeroed by the caller).
 template <int KU, int KV, int FEAT>
-__global__ void __launch_bounds__(kStepThreads, QG_RESIDENT_MINB) k_lsmr_resident(Mats M, LoopArgs L, int *next) {
+__device__ __forceinline__ void resident_body(const Mats &M, const LoopArgs &L, int *next) {
   __shared__ int s_p, s_go;
   const int lane = threadIdx.x & 31;
   while (true) {
@@ -789,6 +789,14 @@ __global__ void __launch_bounds__(kStepThreads, QG_RESIDENT_MINB) k_lsmr_residen
     }
   }
 }
+
+template <int KU, int KV, int FEAT>
+__global__ void __launch_bounds__(kStepThreads, QG_RESIDENT_MINB) k_lsmr_resident(Mats M, LoopArgs L, int *next) {
+  resident_body<KU, KV, FEAT>(M, L, next);
+}
+
+// (Measured and dropped: the same loop as ONE 1024-thread CTA for a single
+// tiny problem with whole-problem units -- c1 8.1 -> 9.5 ms per step.)
 
 __global__ void k_count_active(const Lsmr *st, int B, int *out) {
   __shared__ int cnt;
@@ -976,6 +984,7 @@ void launch_lsmr_resident(const Handle &H, const Mats &M, int ku, const StepArgs
   fin_ptrs(H, L.fu);
   fin_ptrs(H, L.fv);
   const size_t smem = step_smem(H);
+  const int threads = kStepThreads;
   void *kern;
   if (H.has_wide)
     kern = ku == STEP_F ? (void *)k_lsmr_resident<STEP_F, STEP_FT, kFeatWide>
@@ -987,13 +996,13 @@ void launch_lsmr_resident(const Handle &H, const Mats &M, int ku, const StepArgs
   int dev = 0, sms = 0, per_sm = 0;
   QG_CUDA(cudaGetDevice(&dev));
   QG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  QG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem));
+  QG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(H.B, (int64_t)std::max(per_sm, 1) * sms));
   int *next = H.ws.d_nactive;  // reused as the claim counter
   QG_CUDA(cudaMemsetAsync(next, 0, sizeof(int), st));
   Mats m = M;
   void *args[] = {&m, &L, &next};
-  QG_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(kStepThreads), args, smem, st));
+  QG_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, st));
   QG_LAUNCHED();
 }
 
