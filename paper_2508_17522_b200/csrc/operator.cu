@@ -172,7 +172,7 @@ constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatFin = 16;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
 
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
-                                            const double *pre = nullptr);
+                                            const double *pre = nullptr, Lsmr *Lsh = nullptr);
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
@@ -477,12 +477,14 @@ __device__ __forceinline__ bool fin_skips(const FinArgs &a, int p) {
 }
 
 // pre: the 2 x kSlots per-problem sums already reduced (CTA-per-problem
-// finalize); else the warp reduces them (all 32 lanes call).
+// finalize); else the warp reduces them (all 32 lanes call).  Lsh: a
+// shared-memory copy of the problem's LSMR state to work on (the caller
+// loads and stores it cooperatively), else the state in global memory.
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
-                                            const double *pre) {
+                                            const double *pre, Lsmr *Lsh) {
   // partials are read L2-coherent (__ldcg): in the fused variant they were
   // written by other CTAs of the same launch
-  Lsmr *L = a.st ? a.st + p : nullptr;
+  Lsmr *L = Lsh ? Lsh : (a.st ? a.st + p : nullptr);
   if (fin_skips(a, p)) return;
   // deterministic per-problem sums of the producers' partials (fixed order)
   double sx[kSlots] = {0, 0, 0, 0}, sy[kSlots] = {0, 0, 0, 0};
@@ -691,6 +693,15 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
   const int p = (int)blockIdx.x;
   if (fin_skips(a, p)) return;  // CTA-uniform
   __shared__ double red[(256 / 32) * 2 * kSlots];
+  // the LSMR state goes to shared memory in one coalesced sweep (the scalar
+  // recurrence then never waits on global memory for it), and back at the end
+  constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
+  static_assert(sizeof(Lsmr) % sizeof(unsigned long long) == 0, "Lsmr is copied as 8-byte words");
+  __shared__ unsigned long long sLw[kLw];
+  Lsmr *Lsh = a.st ? reinterpret_cast<Lsmr *>(sLw) : nullptr;
+  const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(a.st + p);
+  if (Lsh)
+    for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = Lg[w];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   double s[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 2
@@ -715,7 +726,12 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
       for (int w = 1; w < nw; ++w) t += red[w * 2 * kSlots + j];
       pre[j] = t;
     }
-    fin_problem(M, a, p, 0, pre);
+    fin_problem(M, a, p, 0, pre, Lsh);
+  }
+  if (Lsh) {
+    __syncthreads();
+    unsigned long long *Lw = reinterpret_cast<unsigned long long *>(a.st + p);
+    for (int w = threadIdx.x; w < kLw; w += blockDim.x) Lw[w] = sLw[w];
   }
 }
 
