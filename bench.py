@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--lsmr-iters", type=int, default=100)
     ap.add_argument("--batch", type=int, default=None, help="override the c5a batch size (per rank)")
     ap.add_argument("--strong", action="store_true", help="c5a: shard ONE batch over the ranks (strong scaling)")
+    ap.add_argument("--row-shards", action="store_true",
+                    help="c5b: the row-partitioned NCCL path even at N=1 (exercises it on one GPU)")
     ap.add_argument("--cpu-sample", type=int, default=None, help="problems in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -112,7 +114,7 @@ def shard_range(total, rank, world):
     return rank * total // world, (rank + 1) * total // world
 
 
-def build_workload(cfg, rank, world, batch_override=None, strong=False):
+def build_workload(cfg, rank, world, batch_override=None, strong=False, force_rows=False):
     """This rank's share of the workload (synthetic, seeded per rank).
 
     Batches of independent problems (c5a) scale WEAK by default: every rank
@@ -130,7 +132,7 @@ def build_workload(cfg, rank, world, batch_override=None, strong=False):
             return bt, synth.directions(bt, seed=2000 + rank), per, hi - lo, "strong"
         bt = synth.generate(cfg, seed=1000 + rank, batch=per)
         return bt, synth.directions(bt, seed=2000 + rank), per * world, per, "weak"
-    if cfg in PARTITIONED and world > 1:
+    if cfg in PARTITIONED and (world > 1 or force_rows):
         # one problem, rows of A split over the ranks; every
         # rank builds the same instance and keeps its rows
         full = synth.generate(cfg, seed=1000)
@@ -251,7 +253,8 @@ def run_ours(args):
     from paper_2508_17522_b200 import _native as N
     from paper_2508_17522_b200 import QCPBatch
 
-    bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch, args.strong)
+    bt, dirs, units_total, units_here, scaling = build_workload(args.config, rank, world, args.batch, args.strong,
+                                                                args.row_shards)
     K = args.lsmr_iters
     kw = dict(atol=0.0, btol=0.0, max_iter=K)
     blocks = bt.blocks  # (kind, dim, order, alpha) per block; shared list objects convert once
@@ -263,8 +266,14 @@ def run_ours(args):
     flush = torch.empty(256 * 2 ** 20 // 8, dtype=torch.float64, device=dev)
     comm = None
     if getattr(bt, "shard", None) is not None:
+        import torch.distributed as tdist
+
         from paper_2508_17522_b200 import dist as qdist
 
+        if not tdist.is_initialized():  # --row-shards at N=1: a one-rank NCCL group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            tdist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
         comm = qdist.Comm.nccl()   # the row-partitioned exchange (NCCL inside the LSMR graphs)
 
     def step_device():
@@ -369,9 +378,16 @@ def run_ours(args):
             "clocks": clk.summary(), "lsmr_iterations_per_s": round(value * 2 * K, 1),
         }
         print(json.dumps(line))
+    if comm is not None:
+        comm.close()
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+    else:
+        import torch.distributed as tdist
+
+        if tdist.is_initialized():  # the --row-shards one-rank group
+            tdist.destroy_process_group()
 
 
 def _blk(b):
