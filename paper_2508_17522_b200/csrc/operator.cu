@@ -41,6 +41,9 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 // receives the row sums of the one or two matrices (second may be unused).
 // WIDE: compile the CTA-per-row path (MODE_WIDE units exist); kept out of the
 // common kernels, whose SELL loops lose ~15% to its extra shared state.
+#ifndef QG_SLICE_CLAIM
+#define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
+#endif
 template <bool WIDE, int UNR, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
@@ -55,10 +58,10 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     __syncthreads();
     while (true) {
       int s = 0;
-      if (lane == 0) s = atomicAdd(&next_slice, 2);
+      if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
       s = __shfl_sync(0xffffffffu, s, 0);
       if (s >= u.s1) break;
-      const int sb = s + 1 < u.s1 ? s + 1 : -1;
+      const int sb = (QG_SLICE_CLAIM == 2 && s + 1 < u.s1) ? s + 1 : -1;
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
       double a1, b1v, a2 = 0.0, b2v = 0.0;
