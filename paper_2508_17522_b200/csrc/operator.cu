@@ -44,6 +44,9 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 #ifndef QG_SLICE_CLAIM
 #define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
 #endif
+#ifndef QG_META_PREFETCH
+#define QG_META_PREFETCH 0  // 1: load the next slice pair's metadata during the current pair (A/B)
+#endif
 template <bool WIDE, int UNR, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
@@ -56,6 +59,43 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     __shared__ int next_slice;
     if (threadIdx.x == 0) next_slice = u.s0;
     __syncthreads();
+#if QG_META_PREFETCH
+    // the next pair is claimed and its metadata (offsets, widths, row map)
+    // loaded while the current pair streams
+    auto claim = [&]() {
+      int s = 0;
+      if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
+      return __shfl_sync(0xffffffffu, s, 0);
+    };
+    struct Pair {
+      SliceMeta m1, m2;
+      int ra, rb;
+    };
+    auto fetch = [&](int s) {
+      Pair q{};
+      const int sb = (QG_SLICE_CLAIM == 2 && s + 1 < u.s1) ? s + 1 : -1;
+      q.m1 = slice_meta(S1, s, sb, lane);
+      if (S2) q.m2 = slice_meta(*S2, s, sb, lane);
+      q.ra = rowof[(int64_t)s * 32 + lane];
+      q.rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
+      return q;
+    };
+    int s = claim();
+    Pair cur{};
+    if (s < u.s1) cur = fetch(s);
+    while (s < u.s1) {
+      const int sn = claim();
+      Pair nxt{};
+      if (sn < u.s1) nxt = fetch(sn);
+      double a1, b1v, a2 = 0.0, b2v = 0.0;
+      sell_dot2<UNR>(S1, cur.m1, x1, x1 + b1, a1, b1v);
+      if (S2) sell_dot2<UNR>(*S2, cur.m2, x2, x2 + b2, a2, b2v);
+      if (cur.ra >= 0) row(cur.ra, a1, a2);
+      if (cur.rb >= 0) row(cur.rb, b1v, b2v);
+      s = sn;
+      cur = nxt;
+    }
+#else
     while (true) {
       int s = 0;
       if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
@@ -70,6 +110,7 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
     }
+#endif
   } else if (WIDE && u.mode == MODE_WIDE) {
     // the whole CTA per CSR row: 4 independent partial sums per thread keep
     // the loads in flight, then a fixed-order warp / CTA reduction

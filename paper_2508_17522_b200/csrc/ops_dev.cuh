@@ -69,13 +69,45 @@ __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t
   else sell_dot2_t<UNR>(S, S.col, sa, sb, lane, vec, acc_a, acc_b);
 }
 
+// Start offsets (this lane) and widths of a slice pair; b absent -> width 0.
+struct SliceMeta {
+  int64_t oa, ob;
+  int wa, wb;
+};
+
+__device__ __forceinline__ SliceMeta slice_meta(const SellView &S, int64_t sa, int64_t sb, int lane) {
+  SliceMeta m;
+  m.oa = S.off[sa] + lane;
+  m.wa = S.w[sa];
+  m.ob = sb >= 0 ? S.off[sb] + lane : 0;
+  m.wb = sb >= 0 ? S.w[sb] : 0;
+  return m;
+}
+
+template <int UNR, class Idx>
+__device__ __forceinline__ void sell_dot2_m(const SellView &S, const Idx *colp, const SliceMeta &m,
+                                            const double *vec, double &acc_a, double &acc_b);
+
+// With metadata loaded ahead (the caller prefetches the next pair's while
+// this one streams).
+template <int UNR>
+__device__ __forceinline__ void sell_dot2(const SellView &S, const SliceMeta &m, const double *vec,
+                                          const double *vec_local, double &acc_a, double &acc_b) {
+  if (S.col16) sell_dot2_m<UNR>(S, S.col16, m, vec_local, acc_a, acc_b);
+  else sell_dot2_m<UNR>(S, S.col, m, vec, acc_a, acc_b);
+}
+
 template <int UNR, class Idx>
 __device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, int64_t sa, int64_t sb, int lane,
                                             const double *vec, double &acc_a, double &acc_b) {
-  const int64_t oa = S.off[sa] + lane;
-  const int wa = S.w[sa];
-  const int64_t ob = sb >= 0 ? S.off[sb] + lane : 0;
-  const int wb = sb >= 0 ? S.w[sb] : 0;
+  sell_dot2_m<UNR>(S, colp, slice_meta(S, sa, sb, lane), vec, acc_a, acc_b);
+}
+
+template <int UNR, class Idx>
+__device__ __forceinline__ void sell_dot2_m(const SellView &S, const Idx *colp, const SliceMeta &m,
+                                            const double *vec, double &acc_a, double &acc_b) {
+  const int64_t oa = m.oa, ob = m.ob;
+  const int wa = m.wa, wb = m.wb;
   const int wm = wa < wb ? wa : wb;
   double a = 0.0, b = 0.0;
   int k = 0;
