@@ -114,18 +114,22 @@ Handle::~Handle() {
 }
 
 // ------------------------------------------------------------ create ----
+// QG_TRACE: per-stage wall time of the batch preparation (syncs the stream at
+// every point; diagnostics only).  what == nullptr resets the clock.
+void trace_point(const char *what, cudaStream_t st) {
+  static const bool on = std::getenv("QG_TRACE") != nullptr;
+  static thread_local std::chrono::steady_clock::time_point t0;
+  if (!on) return;
+  cudaStreamSynchronize(st);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (what) std::fprintf(stderr, "[qg] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+  t0 = t1;
+}
+
 struct Tracer {
-  bool on;
   cudaStream_t st;
-  std::chrono::steady_clock::time_point t0;
-  explicit Tracer(cudaStream_t s) : on(std::getenv("QG_TRACE") != nullptr), st(s), t0(std::chrono::steady_clock::now()) {}
-  void operator()(const char *what) {
-    if (!on) return;
-    cudaStreamSynchronize(st);
-    auto t1 = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[qg] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
-    t0 = t1;
-  }
+  explicit Tracer(cudaStream_t s) : st(s) { trace_point(nullptr, st); }
+  void operator()(const char *what) { trace_point(what, st); }
 };
 
 static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {

@@ -321,6 +321,7 @@ void ConeTable::build(const qg_cone_block *blocks, const int64_t *nblocks, const
   units.reserve(unit_ptr[nprob]);
   for (auto &v : part) units.insert(units.end(), v.begin(), v.end());
   nblk = (int64_t)h_blk.size();
+  trace_point("  cone table: host passes", st);
   d_blk = dev_alloc<BlockInfo>(h_blk.size());
   QG_CUDA(cudaMemcpyAsync(d_blk, h_blk.data(), sizeof(BlockInfo) * h_blk.size(), cudaMemcpyHostToDevice, st));
   d_units = dev_alloc<Unit>(units.size());

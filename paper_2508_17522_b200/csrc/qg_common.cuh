@@ -27,6 +27,7 @@ struct Error {
 };
 
 void set_error(int code, const std::string &msg);
+void trace_point(const char *what, cudaStream_t st);  // QG_TRACE diagnostics (api.cu)
 int fail(int code, const std::string &msg);
 void count_launch(int n = 1);
 

@@ -194,6 +194,7 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
     }
   }
   QG_CUDA(cudaMemcpyAsync(d_units, units.data(), sizeof(Unit) * units.size(), cudaMemcpyHostToDevice, st));
+  trace_point("  sell side: unit modes + upload", st);
   *rowof_out = dev_alloc<int32_t>(32 * std::max<int64_t>(ns, 1));
   if (ns == 0 || nrows == 0) return ns;
 
@@ -227,9 +228,11 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
     d_b2 = dev_alloc<int32_t>(ns);
     QG_CUDA(cudaMemcpyAsync(d_b2, slice_b2.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
   }
+  trace_point("  sell side: sort + slice meta", st);
   fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, use16, st);
   if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, use16, st);
   QG_CUDA(cudaStreamSynchronize(st));
+  trace_point("  sell side: fill", st);
   dev_free(keys); dev_free(keys_s); dev_free(rows); dev_free(rows_s); dev_free(tmp);
   dev_free(d_pos); dev_free(d_n); dev_free(w1); dev_free(w2); dev_free(d_b1); dev_free(d_b2);
   return ns;
