@@ -235,7 +235,9 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   const bool isx = ui < M.nxu;
   const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];  // preparation-time data: before the PDL wait
   const int p = u.prob;
+  const Embed E = M.emb[p];                            // (also preparation-time)
   pdl_wait();  // the previous kernel's vectors / LSMR state are complete past this point
+  const double wN = a.in[M.NX + M.NY + p];             // issued with the LSMR-state loads below
   double s_in, c_out;
   if (!lsmr_runs(a, p, s_in, c_out)) {  // CTA-uniform
     // a skipped v-step (beta = 0) still runs its finalize recurrences
@@ -246,9 +248,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     }
     return;
   }
-  const Embed E = M.emb[p];
   const double *inX = a.in, *inY = a.in + M.NX;
-  const double wN = a.in[M.NX + M.NY + p];
   double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
 
   // deferred vector update of the previous iteration over the unit's own rows
