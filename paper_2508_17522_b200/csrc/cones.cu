@@ -165,8 +165,12 @@ size_t ConeTable::psd_smem_prep() const {
 }
 
 size_t ConeTable::psd_smem_apply() const {
-  const int dp = (max_psd_order + 3) & ~3;  // psd_pad (dpi_dev.cuh)
-  return (size_t)4 * dp * (dp + 1) * sizeof(double);
+#if QG_PSD_DMMA
+  const int dp = (max_psd_order + 7) & ~7, ld = dp + 4;  // psd_pad / psd_ld (dpi_dev.cuh)
+#else
+  const int dp = (max_psd_order + 3) & ~3, ld = dp + 1;
+#endif
+  return (size_t)3 * dp * ld * sizeof(double);  // V, S (= W), T: psd_apply_cta
 }
 
 void ConeTable::prepare(const double *z, double *proj, int dual_mode, bool want_deriv, cudaStream_t st) {

@@ -82,6 +82,59 @@ __device__ __forceinline__ void mm_tiles(int d, bool lower, FA a, FB b, FO out) 
   }
 }
 
+// d x d product on the FP64 tensor cores (mma.sync m8n8k4 f64): operands in
+// shared memory, element (i, k) of A at A[i*ai + k*ak], (k, j) of B at
+// B[k*bk + j*bj], zero-padded to nt*8 rows / columns.  Each warp owns up to
+// four 8x8 output tiles at a time (independent accumulator chains); lower =
+// only tiles with tj <= ti.  out(i, j, c) for every element of the owned
+// tiles, padding included (the callers filter).  Fragment layouts (PTX ISA,
+// m8n8k4 .f64): A[lane/4][lane%4], B[lane%4][lane/4], C[lane/4][2*(lane%4)+e].
+__device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <class FO>
+__device__ __forceinline__ void mm_dmma(int nt, bool lower, const double *A, int ai, int ak, const double *B, int bk,
+                                        int bj, FO out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  const int fr = lane >> 2, fc = lane & 3;
+  const int ntile = lower ? nt * (nt + 1) / 2 : nt * nt;
+  for (int t0 = warp * 4; t0 < ntile; t0 += nw * 4) {
+    int ti[4], tj[4];
+    double c0[4], c1[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int t = t0 + q, i = 0;
+      if (lower) {
+        while (t > i) t -= ++i;  // row-major lower-triangle enumeration
+      } else {
+        i = t % nt;
+        t /= nt;
+      }
+      ti[q] = t0 + q < ntile ? i : -1;
+      tj[q] = t;
+      c0[q] = c1[q] = 0.0;
+    }
+    for (int k = 0; k < nt * 8; k += 4) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (ti[q] >= 0) {
+          const double a = A[(ti[q] * 8 + fr) * ai + (k + fc) * ak];
+          const double b = B[(k + fc) * bk + (tj[q] * 8 + fr) * bj];
+          dmma_8x8x4(c0[q], c1[q], a, b);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (ti[q] >= 0) {
+        out(ti[q] * 8 + fr, tj[q] * 8 + 2 * fc, c0[q]);
+        out(ti[q] * 8 + fr, tj[q] * 8 + 2 * fc + 1, c1[q]);
+      }
+  }
+}
+
 // PSD applier (cones.py:791-793): out = svec(V (B o (V' smat(in) V)) V'),
 // evaluated as V' (S V).  CTA-wide; smem holds 4 padded (d x (d+1))
 // matrices (leading dimension d+1 breaks the column-stride bank conflicts).
@@ -90,9 +143,22 @@ __device__ __forceinline__ void mm_tiles(int d, bool lower, FA a, FB b, FO out) 
 // register tiles (up to 4 wide) never leave the arrays; V'T V and the final product are
 // symmetric, so only their lower triangles are computed (3 d^3 instead of
 // 4 d^3 FMAs; c4: 512 blocks of order 32 per F' step).
+// The products run on the FP64 tensor cores (mm_dmma; matrices padded to a
+// multiple of 8, leading dimension dp + 4 = 4 mod 16 doubles: both fragment
+// orientations hit every bank pair exactly twice).  QG_PSD_DMMA=0 builds the
+// CUDA-core register-tile path instead (padding 4, leading dimension dp + 1).
+// c4 F' (512 PSD(32) blocks per step): CUDA-core 2x2 tiles 0.137 ms (4x2
+// 0.145, 4x4 0.325 at 40 registers).
+#ifndef QG_PSD_DMMA
+#define QG_PSD_DMMA 1
+#endif
+#if QG_PSD_DMMA
+static __device__ __forceinline__ int psd_pad(int d) { return (d + 7) & ~7; }
+static __device__ __forceinline__ int psd_ld(int dp) { return dp + 4; }
+#else
 static __device__ __forceinline__ int psd_pad(int d) { return (d + 3) & ~3; }
-// Register tile of the PSD products.  c4 F' (512 PSD(32) blocks): 2x2 0.137
-// ms, 4x2 0.145 ms, 4x4 0.325 ms (the F' step runs at 40 registers).
+static __device__ __forceinline__ int psd_ld(int dp) { return dp + 1; }
+#endif
 #ifndef PSD_TI
 #define PSD_TI 2
 #endif
@@ -100,14 +166,18 @@ static __device__ __forceinline__ int psd_pad(int d) { return (d + 3) & ~3; }
 #define PSD_TJ 2
 #endif
 
+// Shared memory: V, S and T (W reuses S, dead after the first product:
+// 3 instead of 4 matrices -> more CTAs per SM for the whole F' step).
+// have_v: V is already in sm from the previous apply of the same block (the
+// F' epilogue applies D Pi twice per block; no product writes V).
 static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
-                                     double *sm) {
-  const int dp = psd_pad(d), ld = dp + 1, sz = dp * ld;
-  double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = sm + 3 * sz;
+                                     double *sm, bool have_v = false) {
+  const int dp = psd_pad(d), ld = psd_ld(dp), sz = dp * ld;
+  double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = S;
   for (int idx = threadIdx.x; idx < dp * dp; idx += blockDim.x) {
     const int i = idx % dp, j = idx / dp;
     const bool in_d = i < d && j < d;
-    V[i + j * ld] = in_d ? Vg[i + j * d] : 0.0;
+    if (!have_v) V[i + j * ld] = in_d ? Vg[i + j * d] : 0.0;
     double s = 0.0;
     if (in_d) {
       const int a = i >= j ? i : j, b = i >= j ? j : i;
@@ -116,9 +186,29 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
     }
     S[i + j * ld] = s;
     T[i + j * ld] = 0.0;
-    W[i + j * ld] = 0.0;
   }
   __syncthreads();
+#if QG_PSD_DMMA
+  const int nt = dp >> 3;
+  // T = S V ; W = (V' T) o B (lower, mirrored) ; T = V W ; out = svec(T V')
+  // (padded rows / columns of every product are zero; only W and out filter)
+  mm_dmma(nt, false, S, 1, ld, V, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
+  __syncthreads();
+  mm_dmma(nt, true, V, ld, 1, T, 1, ld, [&](int i, int j, double c) {
+    if (i >= j && i < d) {
+      const double w = Bg[i + j * d] * c;
+      W[i + j * ld] = w;
+      W[j + i * ld] = w;
+    }
+  });
+  __syncthreads();
+  mm_dmma(nt, false, V, 1, ld, W, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
+  __syncthreads();
+  mm_dmma(nt, true, T, 1, ld, V, ld, 1, [&](int i, int j, double c) {
+    if (i >= j && i < d) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
+  });
+  __syncthreads();
+#else
   // T = S V
   mm_tiles<PSD_TI, PSD_TJ>(d, false, [&](int i, int k) { return S[i + k * ld]; }, [&](int k, int j) { return V[k + j * ld]; },
                  [&](int i, int j, double c) { T[i + j * ld] = c; });
@@ -143,11 +233,13 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
                    if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
                  });
   __syncthreads();
+#endif
 }
 
 // Apply D Pi to the unit's rows.  in/out are indexed by (row - unit.row0);
 // they may live in global memory (written by this CTA before a barrier).
-static __device__ void dpi_apply_unit(const DpiView &dv, const Unit &u, const double *in, double *out, double *sm) {
+static __device__ void dpi_apply_unit(const DpiView &dv, const Unit &u, const double *in, double *out, double *sm,
+                                      bool have_v = false) {
   if (u.cls == CLS_ELEM) {
     const BlockInfo b = dv.blk[u.blk0];
     for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
@@ -165,7 +257,7 @@ static __device__ void dpi_apply_unit(const DpiView &dv, const Unit &u, const do
     const BlockInfo b = dv.blk[u.blk0];
     const double *V = dv.psd + b.param;
     const int d = b.order;
-    psd_apply_cta(V, V + d * d, d, in + (b.row - u.row0), out + (b.row - u.row0), sm);
+    psd_apply_cta(V, V + d * d, d, in + (b.row - u.row0), out + (b.row - u.row0), sm, have_v);
   } else {  // CLS_TRI
     for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
       const BlockInfo b = dv.blk[k];

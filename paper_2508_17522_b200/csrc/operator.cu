@@ -372,7 +372,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
         dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
         for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
         __syncthreads();
-        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm);
+        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm, true);  // V still in sm
       }
     }
   }
