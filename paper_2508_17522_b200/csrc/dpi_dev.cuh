@@ -166,6 +166,28 @@ static __device__ __forceinline__ int psd_ld(int dp) { return dp + 1; }
 #define PSD_TJ 2
 #endif
 
+// Asynchronous copy of a PSD unit's eigenvector matrix V (preparation-time
+// data) into its shared-memory slot, issued at the start of the F' step so
+// the load latency hides behind the unit's SpMV pass; psd_apply_cta(...,
+// have_v = true) then waits for it.  No-op for other units.
+static __device__ __forceinline__ void psd_prefetch_v(const DpiView &dv, const Unit &u, double *sm) {
+  if (u.cls != CLS_PSD) return;
+  const BlockInfo b = dv.blk[u.blk0];
+  const int d = b.order, dp = psd_pad(d), ld = psd_ld(dp);
+  const double *Vg = dv.psd + b.param;
+  for (int idx = threadIdx.x; idx < dp * dp; idx += blockDim.x) {
+    const int i = idx % dp, j = idx / dp;
+    double *dst = sm + i + j * ld;
+    if (i < d && j < d) {
+      const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(Vg + i + j * d) : "memory");
+    } else {
+      *dst = 0.0;
+    }
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 // Shared memory: V, S and T (W reuses S, dead after the first product:
 // 3 instead of 4 matrices -> more CTAs per SM for the whole F' step).
 // have_v: V is already in sm from the previous apply of the same block (the
@@ -174,6 +196,7 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
                                      double *sm, bool have_v = false) {
   const int dp = psd_pad(d), ld = psd_ld(dp), sz = dp * ld;
   double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = S;
+  if (have_v) asm volatile("cp.async.wait_all;" ::: "memory");  // psd_prefetch_v (barrier below)
   for (int idx = threadIdx.x; idx < dp * dp; idx += blockDim.x) {
     const int i = idx % dp, j = idx / dp;
     const bool in_d = i < d && j < d;

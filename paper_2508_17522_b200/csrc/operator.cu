@@ -209,6 +209,9 @@ constexpr int kStepThreads = 128;
 #ifndef QG_FT_UNROLL
 #define QG_FT_UNROLL 2
 #endif
+#ifndef QG_PSD_PREFETCH
+#define QG_PSD_PREFETCH 1
+#endif
 #ifndef QG_RESIDENT_MINB
 #define QG_RESIDENT_MINB 8
 #endif
@@ -236,6 +239,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];  // preparation-time data: before the PDL wait
   const int p = u.prob;
   const Embed E = M.emb[p];                            // (also preparation-time)
+  if (KIND == STEP_FT && !isx && QG_PSD_PREFETCH) psd_prefetch_v(M.dpi, u, sm);  // V behind the SpMV pass
   pdl_wait();  // the previous kernel's vectors / LSMR state are complete past this point
   const double wN = a.in[M.NX + M.NY + p];             // issued with the LSMR-state loads below
   double s_in, c_out;
@@ -246,6 +250,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
       const int first = M.xu_ptr[p] < M.xu_ptr[p + 1] ? (int)M.xu_ptr[p] : M.nxu + (int)M.yu_ptr[p];
       if (ui == first) fin_problem(M, a.fin, p, (int)threadIdx.x);
     }
+    if (KIND == STEP_FT && QG_PSD_PREFETCH) asm volatile("cp.async.wait_all;" ::: "memory");  // (prefetch)
     return;
   }
   const double *inX = a.in, *inY = a.in + M.NX;
@@ -369,7 +374,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
         soc_epilogue(M.dpi, u, tY, fin_row, outY, a.dpout);
       } else {
         // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
-        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm);
+        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm, QG_PSD_PREFETCH && u.cls == CLS_PSD);
         for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
         __syncthreads();
         if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm, true);  // V still in sm
