@@ -187,7 +187,10 @@ def alg_bytes(bt):
             elif k in ("exp", "dexp", "pow", "dpow"):
                 ntri += 1
     s_dpi = 8 * NY + 12 * nsoc + 76 * ntri + psd
-    return {"F": mats + vec, "FT": mats + vec + 8 * NY + 2 * s_dpi}
+    # PSD D Pi apply = V'WV, Hadamard with B, V S V': 4 dense d x d x d products
+    # (2 d^3 flops each); the F' step applies it twice per block
+    psd_flops = sum(2 * 4 * 2 * o ** 3 for blocks in bt.blocks for (k, d, o, a) in blocks if k == "psd")
+    return {"F": mats + vec, "FT": mats + vec + 8 * NY + 2 * s_dpi, "FT_psd_flops": psd_flops}
 
 
 # ---------------------------------------------------------------- clocks --
@@ -356,6 +359,16 @@ def run_ours(args):
             "alg_bytes_per_launch": ab["FT"], "launch_ms": round(t_ft, 4),
             "f_step": {"achieved": round(ab["F"] / (t_f / 1e3) / 1e9, 1), "launch_ms": round(t_f, 4),
                        "alg_bytes_per_launch": ab["F"]}}
+    if ab["FT_psd_flops"]:
+        # the PSD share of F' is FP64-compute-shaped: its flops over the whole
+        # F' launch time, against cuBLAS DGEMM measured here (a lower bound on
+        # the PSD kernels' own rate, since the launch also streams the SpMVs)
+        fp64 = _dgemm_tflops(dev)
+        ach_f = ab["FT_psd_flops"] / (t_ft / 1e3) / 1e12
+        roof["psd_fp64"] = {"achieved": round(ach_f, 3), "peak": round(fp64, 2), "unit": "TFLOP/s",
+                            "peak_source": "cuBLAS DGEMM 8192^3 fp64, measured in this run",
+                            "frac": round(ach_f / fp64, 4), "flops_per_launch": ab["FT_psd_flops"],
+                            "products": "mma.sync m8n8k4 f64 (DMMA)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # contract: N=1 only
@@ -409,6 +422,25 @@ def _peaks():
             return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     except (OSError, KeyError, ValueError):
         return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def _dgemm_tflops(dev, n=8192, reps=5):
+    """Measured fp64 GEMM rate (cuBLAS DGEMM, CUDA events, best of reps):
+    the FP64 tensor-core roofline the PSD products are compared with."""
+    import torch
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    torch.matmul(a, b)
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * n ** 3 / (best / 1e3) / 1e12
 
 
 def _traffic(cfg, alg):

@@ -39,7 +39,13 @@ def _newer(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose=False, force=False):
+def build(verbose=False, force=False, out=None, defines=()):
+    """Compile every source and link libqcpgrad.so into ``out`` (default ``_lib/``).
+
+    ``defines`` (e.g. ``["QG_PSD_DMMA=0"]``) builds an A/B variant of the
+    compile-time switches; load it with ``QG_LIB_PATH``.
+    """
+    OUT = out or globals()["OUT"]
     os.makedirs(OUT, exist_ok=True)
     headers = [os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "qcpgrad.h"))
@@ -49,7 +55,7 @@ def build(verbose=False, force=False):
         s = os.path.join(SRC, src)
         o = os.path.join(OUT, src.replace(".cu", ".o"))
         if force or _newer(o, [s] + headers):
-            cmd = [nvcc()] + NVCC_FLAGS + ["-c", s, "-o", o]
+            cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-c", s, "-o", o]
             if verbose:
                 print(" ".join(cmd))
             r = subprocess.run(cmd, capture_output=True, text=True)
@@ -70,4 +76,8 @@ def build(verbose=False, force=False):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    # python -m paper_2508_17522_b200.build [-v] [-f] [--out DIR] [-D NAME=VAL ...]
+    a = sys.argv[1:]
+    out = a[a.index("--out") + 1] if "--out" in a else None
+    defs = [a[i + 1] for i, x in enumerate(a) if x == "-D"]
+    print(build(verbose="-v" in a, force="-f" in a, out=out, defines=defs))

@@ -41,13 +41,19 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 // receives the row sums of the one or two matrices (second may be unused).
 // WIDE: compile the CTA-per-row path (MODE_WIDE units exist); kept out of the
 // common kernels, whose SELL loops lose ~15% to its extra shared state.
+#ifndef QG_ROWS32
+#define QG_ROWS32 2  // CSR rows walked together per warp on the warp-per-row path, F step (1: one at a time)
+#endif
+#ifndef QG_ROWS32_FT
+#define QG_ROWS32_FT 1  // same for the F' step: c2 / c3 / c4 F 0.0086 / 0.0320 / 0.0325 -> 0.0080 / 0.0297 /
+#endif                  // 0.0329 ms with 2 rows; F' c4 0.0847 -> 0.0874 (4 rows: slower everywhere)
 #ifndef QG_SLICE_CLAIM
 #define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
 #endif
 #ifndef QG_META_PREFETCH
 #define QG_META_PREFETCH 0  // 1: load the next slice pair's metadata during the current pair (A/B)
 #endif
-template <bool WIDE, int UNR, class RowFn>
+template <bool WIDE, int UNR, int ROWS32, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
@@ -138,12 +144,33 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
   } else if (G == 32) {
     // warp per row with a compile-time lane stride: the loop unrolls into
     // independent loads (a runtime stride measured 7x slower on C5b)
-    for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
-      double s1 = row_dot32(rp1, c1, v1, x1, r, lane);
-      double s2 = rp2 ? row_dot32(rp2, c2, v2, x2, r, lane) : 0.0;
-      s1 = warp_sum(s1);
-      s2 = warp_sum(s2);
-      if (lane == 0) row(r, s1, s2);
+    if constexpr (ROWS32 > 1) {
+      // ROWS32 rows of the warp's row sequence at once (same rows, same
+      // order of row() calls as the one-row loop)
+      const int nw = (int)(blockDim.x >> 5);
+      constexpr int R = ROWS32;
+      for (int r0 = u.row0 + warp; r0 < u.row1; r0 += R * nw) {
+        double s1[R], s2[R];
+        row_dot32_multi<R>(rp1, c1, v1, x1, r0, nw, u.row1, lane, s1);
+        if (rp2) row_dot32_multi<R>(rp2, c2, v2, x2, r0, nw, u.row1, lane, s2);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          s1[j] = warp_sum(s1[j]);
+          s2[j] = rp2 ? warp_sum(s2[j]) : 0.0;
+        }
+        if (lane == 0)
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (r0 + j * nw < u.row1) row(r0 + j * nw, s1[j], s2[j]);
+      }
+    } else {
+      for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
+        double s1 = row_dot32(rp1, c1, v1, x1, r, lane);
+        double s2 = rp2 ? row_dot32(rp2, c2, v2, x2, r, lane) : 0.0;
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (lane == 0) row(r, s1, s2);
+      }
     }
   } else {
     // G lanes per CSR row (G from the average row length of the matrices),
@@ -232,6 +259,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
   constexpr bool kFin = (FEAT & kFeatFin) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
+  constexpr int kRows32 = KIND == STEP_F ? QG_ROWS32 : QG_ROWS32_FT;  // rows per warp, warp-per-row CSR
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -276,7 +304,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
-      for_rows<kWide, kUnr>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
+      for_rows<kWide, kUnr, kRows32>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
                u.lanes, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
@@ -301,10 +329,10 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                acc[2] += o * o;
              };
     if (kDist && a.xmode == X_FINISH)
-      for_rows<kWide, kUnr>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
-      for_rows<kWide, kUnr>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
+      for_rows<kWide, kUnr, kRows32>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
                M.xoff[p], M.yoff[p], xrow);
     if (kDist && !M.x_owner)
 #pragma unroll
@@ -313,7 +341,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
-      for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
@@ -328,7 +356,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
       double *tY = a.tY;
-      for_rows<kWide, kUnr>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
                [&](int r, double s, double) {
                  tY[r] = (s - wN * M.b[r]) - inY[r];

@@ -160,6 +160,37 @@ __device__ __forceinline__ double row_dot32(const int32_t *rp, const int32_t *co
   return s;
 }
 
+// R rows per warp at once (rows r0, r0 + stride, ...; valid ones only): one
+// loop walks all R rows together, so the R rows' column / value loads and
+// vector gathers are in flight at the same time instead of R serial
+// load -> gather chains.  Each row still sums its lane's entries k, k + 32,
+// ... in the same order as row_dot32, so the row sums are bit-identical.
+template <int R>
+__device__ __forceinline__ void row_dot32_multi(const int32_t *rp, const int32_t *col, const double *val,
+                                                const double *vec, int r0, int stride, int r_end, int lane,
+                                                double (&s)[R]) {
+  int k[R], ke[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int r = r0 + j * stride;
+    const bool ok = r < r_end;
+    k[j] = ok ? rp[r] + lane : 0;
+    ke[j] = ok ? rp[r + 1] : 0;
+    s[j] = 0.0;
+  }
+  for (;;) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (k[j] < ke[j]) {
+        s[j] += val[k[j]] * vec[col[k[j]]];
+        k[j] += 32;
+        any = true;
+      }
+    if (!any) break;
+  }
+}
+
 // Group-of-G sum inside a warp (G power of two, runtime).
 __device__ __forceinline__ double gsum(double v, int G) {
   for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
