@@ -47,13 +47,19 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 #ifndef QG_ROWS32_FT
 #define QG_ROWS32_FT 1  // same for the F' step: c2 / c3 / c4 F 0.0086 / 0.0320 / 0.0325 -> 0.0080 / 0.0297 /
 #endif                  // 0.0329 ms with 2 rows; F' c4 0.0847 -> 0.0874 (4 rows: slower everywhere)
+#ifndef QG_ROWSG
+#define QG_ROWSG 2  // row groups walked together per warp on the G-lanes-per-row path, F step:
+#endif                // c2 / c3 F 0.0079 / 0.0298 -> 0.0076 / 0.0290 ms with 2 (4: 0.0078 / 0.0297)
+#ifndef QG_ROWSG_FT
+#define QG_ROWSG_FT 4  // same, F' step: c5b F' 0.2671 -> 0.2595 ms with 4 (2: 0.2676),
+#endif                   // c3 0.0272 -> 0.0276, c2 / c4 neutral
 #ifndef QG_SLICE_CLAIM
 #define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
 #endif
 #ifndef QG_META_PREFETCH
 #define QG_META_PREFETCH 0  // 1: load the next slice pair's metadata during the current pair (A/B)
 #endif
-template <bool WIDE, int UNR, int ROWS32, class RowFn>
+template <bool WIDE, int UNR, int ROWS32, int ROWSG, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
                                          const double *v1, const int32_t *rp2, const int32_t *c2,
@@ -176,6 +182,28 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     // G lanes per CSR row (G from the average row length of the matrices),
     // loops warp-uniform so every lane reaches the shuffles
     const int lg = lane & (G - 1), gpw = 32 / G, nw = (int)(blockDim.x >> 5);
+    if constexpr (ROWSG > 1) {
+      // ROWSG row groups of the warp's sequence at once; each lane still
+      // calls row() for its rows in the one-group order
+      constexpr int R = ROWSG;
+      const int stride = nw * gpw;
+      for (int base = u.row0 + warp * gpw; base < u.row1; base += R * stride) {
+        const int r = base + lane / G;
+        double s1[R], s2[R];
+        row_dot_multi<R>(rp1, c1, v1, x1, r, stride, u.row1, lg, G, s1);
+        if (rp2) row_dot_multi<R>(rp2, c2, v2, x2, r, stride, u.row1, lg, G, s2);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+          s1[j] = gsum(s1[j], G);
+          s2[j] = rp2 ? gsum(s2[j], G) : 0.0;
+        }
+        if (lg == 0)
+#pragma unroll
+          for (int j = 0; j < R; ++j)
+            if (r + j * stride < u.row1) row(r + j * stride, s1[j], s2[j]);
+      }
+      return;
+    }
     for (int base = u.row0 + warp * gpw; base < u.row1; base += nw * gpw) {
       const int r = base + lane / G;
       const bool valid = r < u.row1;
@@ -260,6 +288,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   constexpr bool kFin = (FEAT & kFeatFin) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
   constexpr int kRows32 = KIND == STEP_F ? QG_ROWS32 : QG_ROWS32_FT;  // rows per warp, warp-per-row CSR
+  constexpr int kRowsG = KIND == STEP_F ? QG_ROWSG : QG_ROWSG_FT;     // row groups per warp, G-lane CSR
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -304,7 +333,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     const double *x2 = KIND == STEP_F ? a.dpin : inY;
     if (kDist && a.xmode == X_PARTIAL) {
       // this rank's A_r' (D Pi w)_2 (F) or A_r' w2 (F') for the X rows
-      for_rows<kWide, kUnr, kRows32>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
+      for_rows<kWide, kUnr, kRows32, kRowsG>(u,M.sAT, nullptr, M.x_rowof, M.AT_rp, M.AT_col, M.AT_val, nullptr, nullptr, nullptr, x2, nullptr,
                u.lanes, M.yoff[p], 0, [&](int r, double s, double) { a.xred[r] = s; });
       return;  // CTA-uniform; the X slots are written by the X_FINISH launch
     }
@@ -329,10 +358,10 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
                acc[2] += o * o;
              };
     if (kDist && a.xmode == X_FINISH)
-      for_rows<kWide, kUnr, kRows32>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32, kRowsG>(u,M.sP, nullptr, M.x_rowof, M.P_rp, M.P_col, M.P_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0, [&](int r, double s1, double) { xrow(r, s1, a.xred[r]); });
     else
-      for_rows<kWide, kUnr, kRows32>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
+      for_rows<kWide, kUnr, kRows32, kRowsG>(u,M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col, M.AT_val, inX, x2, u.lanes,
                M.xoff[p], M.yoff[p], xrow);
     if (kDist && !M.x_owner)
 #pragma unroll
@@ -341,7 +370,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     double *outY = a.out + M.NX;
     const double *oldY = a.old ? a.old + M.NX : nullptr;
     if (KIND == STEP_F) {
-      for_rows<kWide, kUnr, kRows32>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32, kRowsG>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
                [&](int r, double s, double) {
                  // out2 = -A w1 + w_N b ; (out - D Pi w + w)/z_N
@@ -356,7 +385,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     } else {
       // pass 1: t = (A w1 - w_N b) - w2  for every row of the unit
       double *tY = a.tY;
-      for_rows<kWide, kUnr, kRows32>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      for_rows<kWide, kUnr, kRows32, kRowsG>(u,M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
                M.xoff[p], 0,
                [&](int r, double s, double) {
                  tY[r] = (s - wN * M.b[r]) - inY[r];

@@ -197,6 +197,34 @@ __device__ __forceinline__ double gsum(double v, int G) {
   return v;
 }
 
+// R rows per lane group at once (rows r0, r0 + stride, ...; rows >= r_end
+// give 0), each summed in row_dot's order (bit-identical row sums).
+template <int R>
+__device__ __forceinline__ void row_dot_multi(const int32_t *rp, const int32_t *col, const double *val,
+                                              const double *vec, int r0, int stride, int r_end, int lane_g, int G,
+                                              double (&s)[R]) {
+  int k[R], ke[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    const int r = r0 + j * stride;
+    const bool ok = r < r_end;
+    k[j] = ok ? rp[r] + lane_g : 0;
+    ke[j] = ok ? rp[r + 1] : 0;
+    s[j] = 0.0;
+  }
+  for (;;) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+      if (k[j] < ke[j]) {
+        s[j] += val[k[j]] * vec[col[k[j]]];
+        k[j] += G;
+        any = true;
+      }
+    if (!any) break;
+  }
+}
+
 // Row dot product by a group of G lanes: sum_k val[k] * vec[col[k]].
 __device__ __forceinline__ double row_dot(const int32_t *rp, const int32_t *col, const double *val,
                                           const double *vec, int r, int lane_g, int G) {
