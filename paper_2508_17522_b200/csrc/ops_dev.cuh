@@ -33,7 +33,27 @@ enum XMode : int { X_FULL = 0, X_PARTIAL = 1, X_FINISH = 2 };
 // Streamed matrix loads (each stored entry is read once per step):
 // read-only and not allocated in L1, so the gathered vectors keep the L1 to
 // themselves (c5a: F 0.462 -> 0.454 ms, F' 0.584 -> 0.574 ms vs __ldcs).
+#ifndef QG_L2_EVICT_FIRST
+#define QG_L2_EVICT_FIRST 0  // 1: also mark the streamed entries evict-first in L2 (A/B)
+#endif
 #ifndef QG_LDCS_LOADS
+#if QG_L2_EVICT_FIRST
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;  // uniform; ptxas keeps it in the load's descriptor
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double ld_stream(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+__device__ __forceinline__ int ld_stream(const int *p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+}
+#else
 __device__ __forceinline__ double ld_stream(const double *p) {
   double v;
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -44,6 +64,7 @@ __device__ __forceinline__ int ld_stream(const int *p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+#endif
 __device__ __forceinline__ unsigned short ld_stream(const unsigned short *p) { return __ldcs(p); }
 #else
 template <class T>
