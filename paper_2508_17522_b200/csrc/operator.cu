@@ -44,6 +44,9 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 #ifndef QG_ROWS32
 #define QG_ROWS32 2  // CSR rows walked together per warp on the warp-per-row path, F step (1: one at a time)
 #endif
+#ifndef QG_ROWS32_SELL
+#define QG_ROWS32_SELL 1  // same, F step of SELL handles (8 CTAs/SM; multi-row walks cost c5a F 0.4515 -> 0.472 ms)
+#endif
 #ifndef QG_ROWS32_FT
 #define QG_ROWS32_FT 1  // same for the F' step: c2 / c3 / c4 F 0.0086 / 0.0320 / 0.0325 -> 0.0080 / 0.0297 /
 #endif                  // 0.0329 ms with 2 rows; F' c4 0.0847 -> 0.0874 (4 rows: slower everywhere)
@@ -282,13 +285,15 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
 // The common variant (0) carries none of them.
 // One work unit (`ui`: X units then Y units) of an operator step, by the
 // whole CTA; the partial-sum slot of the unit is part[ui].
-template <int KIND, int FEAT>
+template <int KIND, int FEAT, bool SELL8 = false>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
   constexpr bool kFin = (FEAT & kFeatFin) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
-  constexpr int kRows32 = KIND == STEP_F ? QG_ROWS32 : QG_ROWS32_FT;  // rows per warp, warp-per-row CSR
-  constexpr int kRowsG = KIND == STEP_F ? QG_ROWSG : QG_ROWSG_FT;     // row groups per warp, G-lane CSR
+  // rows per warp, warp-per-row CSR; SELL8 = the 8-CTA/SM SELL F instantiation
+  constexpr int kRows32 = KIND == STEP_F ? (SELL8 ? QG_ROWS32_SELL : QG_ROWS32) : QG_ROWS32_FT;
+  // row groups per warp, G-lane CSR (the SELL F kernel: one group, as for ROWS32)
+  constexpr int kRowsG = KIND == STEP_F ? (SELL8 ? 1 : QG_ROWSG) : QG_ROWSG_FT;
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
   __shared__ double red[kWarps * kSlots];
@@ -465,7 +470,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
 
 template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
-  step_unit<KIND, FEAT>(M, a, (int)blockIdx.x);
+  step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, (int)blockIdx.x);
 }
 
 // -------------------------------------------------------------- update --
