@@ -279,10 +279,12 @@ def run_ours(args):
             tdist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
         comm = qdist.Comm.nccl()   # the row-partitioned exchange (NCCL inside the LSMR graphs)
 
+    last_diags = {}
+
     def step_device():
         b = QCPBatch.from_device(*sizes, dev_in, comm=comm)
-        b.jvp_device(ddir["dP"], ddir["dA"], ddir["dq"], ddir["db"], **kw)
-        b.vjp_device(ddir["dx"], ddir["dy"], ddir["ds"], **kw)
+        last_diags["jvp"] = b.jvp_device(ddir["dP"], ddir["dA"], ddir["dq"], ddir["db"], **kw)[-1]
+        last_diags["vjp"] = b.vjp_device(ddir["dx"], ddir["dy"], ddir["ds"], **kw)[-1]
         return b
 
     def timed(fn, steps):
@@ -313,6 +315,13 @@ def run_ours(args):
     ms = max_over_ranks(dist, ms, dev)
     ms_per_step = ms / args.steps
     value = units_total / (ms_per_step / 1e3)
+    # the fixed cap must really run K iterations for every problem (with
+    # atol=btol=0 the machine-precision stop tests can still end a solve
+    # early, which would inflate evals/s): checked on the last timed step
+    its = {k: [int(d.iterations) for d in v] for k, v in last_diags.items()}
+    its_summary = {k: {"min": min(v), "mean": round(sum(v) / len(v), 2), "max": max(v)} for k, v in its.items()}
+    if any(i != K for v in its.values() for i in v):
+        print(f"bench.py: WARNING: not every LSMR solve ran K={K} iterations: {its_summary}", file=sys.stderr)
 
     # end to end through the host-buffer API: H2D of data + directions, D2H of outputs
     e2e = None
@@ -389,6 +398,7 @@ def run_ours(args):
                                        if args.config in BATCH else f"replicas x{world}")},
             "e2e": e2e, "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": cpu,
             "clocks": clk.summary(), "lsmr_iterations_per_s": round(value * 2 * K, 1),
+            "lsmr_iterations": its_summary,
         }
         print(json.dumps(line))
     if comm is not None:
@@ -454,7 +464,7 @@ def _traffic(cfg, alg):
 
 
 # --------------------------------------------------------- CPU reference --
-def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=None):
+def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=None, impl=None):
     """Problems in the CPU sample: ``--cpu-sample`` if given, else one per
     core, grown (in whole rounds over the cores, up to the batch) until the
     sample is about ``target_s`` seconds of CPU work."""
@@ -464,10 +474,10 @@ def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=N
     base = cores if batched else 1
     if target_s is None or bt is None or not batched:
         return base
-    from oracle import cpu_bench
-
+    if impl is None:
+        impl = cpu_impl()[0]
     base = min(base, bt.B)
-    secs = cpu_bench.time_sample(bt, dirs, K, range(base), min(cores, base))
+    secs = impl.time_sample(bt, dirs, K, range(base), min(cores, base))
     rounds = max(1, int(target_s / max(secs, 1e-3)))
     return min(bt.B, base * rounds)
 
@@ -475,26 +485,41 @@ def cpu_sample_size(args, scaling, cores, bt=None, dirs=None, K=None, target_s=N
 EXTRAPOLATE = {"c3": 4, "c4": 6, "c5b": 3}   # single-problem configs whose K=100 CPU eval takes minutes
 
 
-def cpu_baseline(bt, dirs, K, args, scaling):
-    """The oracle (the reference algorithm restated) on the host cores."""
+def cpu_impl():
+    """The CPU implementation timed beside the GPU: the unmodified reference
+    installed in baseline/_ref (conegrad, compiled backend; kind "reference")
+    when it imports, else the oracle port (kind "port")."""
+    from baseline import ref_cpu
+
+    ok, why = ref_cpu.available()
+    if ok:
+        return ref_cpu, "reference", f"conegrad 0.1.0 from baseline/_ref ({why} SpMV backend), check=False"
     from oracle import cpu_bench
 
+    return cpu_bench, "port", f"oracle port (reference unavailable: {why})"
+
+
+def cpu_baseline(bt, dirs, K, args, scaling):
+    """The reference's CPU path on the host cores (rank 0, N=1)."""
+    from oracle import cpu_bench
+
+    impl, kind, desc = cpu_impl()
     cores = cpu_bench.host_cores()
     nprob = bt.B
     if args.config in EXTRAPOLATE:
         ks = EXTRAPOLATE[args.config]
-        est, t0, per_iter = cpu_bench.extrapolated_eval_seconds(bt, dirs, 0, K, ks)
-        return {"value": round(1.0 / est, 6), "unit": "evals/s", "cores": 1, "kind": "port",
+        est, t0, per_iter = impl.extrapolated_eval_seconds(bt, dirs, 0, K, ks)
+        return {"value": round(1.0 / est, 6), "unit": "evals/s", "cores": 1, "kind": kind,
                 "sample": f"1 problem, jvp+vjp timed at caps 0 and {ks} (setup {t0:.2f} s, "
                           f"{per_iter:.3f} s per LSMR iteration of jvp+vjp) extrapolated to K={K}; "
-                          f"1 process x 1 thread ({cpu_bench.cpu_model()})",
+                          f"1 process x 1 thread ({cpu_bench.cpu_model()}); {desc}",
                 "seconds": round(est, 2)}
     sample = min(cpu_sample_size(args, scaling, cores, bt, dirs, K, target_s=12.0), nprob)
     workers = min(cores, sample)
-    secs = cpu_bench.time_sample(bt, dirs, K, range(sample), workers)
-    return {"value": round(sample / secs, 4), "unit": "evals/s", "cores": workers, "kind": "port",
+    secs = impl.time_sample(bt, dirs, K, range(sample), workers)
+    return {"value": round(sample / secs, 4), "unit": "evals/s", "cores": workers, "kind": kind,
             "sample": f"{sample} of {nprob} problems of this rank's workload, jvp+vjp at K={K}, "
-                      f"{workers} processes x 1 thread ({cpu_bench.cpu_model()})",
+                      f"{workers} processes x 1 thread ({cpu_bench.cpu_model()}); {desc}",
             "seconds": round(secs, 2)}
 
 
@@ -504,15 +529,19 @@ def run_reference(args):
         return  # rank 0 alone times the CPU reference
     from oracle import cpu_bench
 
+    impl, kind, desc = cpu_impl()
     bt, dirs, units_total, units_here, scaling = build_workload(args.config, 0, 1, args.batch)
     K = args.lsmr_iters
     cores = cpu_bench.host_cores()
-    sample = min(cpu_sample_size(args, scaling, cores, bt, dirs, K, target_s=6.0), bt.B)
+    sample = min(cpu_sample_size(args, scaling, cores, bt, dirs, K, target_s=6.0, impl=impl), bt.B)
     workers = min(cores, sample)
     for _ in range(args.warmup):
-        cpu_bench.time_sample(bt, dirs, K, range(sample), workers)
-    secs = [cpu_bench.time_sample(bt, dirs, K, range(sample), workers) for _ in range(args.steps)]
+        impl.time_sample(bt, dirs, K, range(sample), workers)
+    its = []
+    secs = [impl.time_sample(bt, dirs, K, range(sample), workers, its) if kind == "reference" else
+            impl.time_sample(bt, dirs, K, range(sample), workers) for _ in range(args.steps)]
     value = sample / (sum(secs) / len(secs))
+    flat = [i for pair in its for i in pair]
     line = {
         "impl": "reference", "metric": "jvp+vjp evals/s", "value": round(value, 4), "unit": "evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -520,11 +549,13 @@ def run_reference(args):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (same generator and seeds as the GPU arm)",
         "config": {"workload": f"{args.config}: {CONFIGS[args.config]}",
                    "lsmr": f"fixed cap K={K} (atol=btol=0)", "sample_problems_per_step": sample},
-        "cpu_baseline": {"value": round(value, 4), "unit": "evals/s", "cores": workers, "kind": "port",
+        "cpu_baseline": {"value": round(value, 4), "unit": "evals/s", "cores": workers, "kind": kind,
                          "sample": f"{sample} problems per step, {workers} processes x 1 thread "
-                                   f"({cpu_bench.cpu_model()})"},
+                                   f"({cpu_bench.cpu_model()}); {desc}"},
         "e2e": {"value": round(value, 4), "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if flat:
+        line["lsmr_iterations"] = {"min": min(flat), "mean": round(sum(flat) / len(flat), 2), "max": max(flat)}
     print(json.dumps(line))
 
 

@@ -6,6 +6,7 @@ The shared library lands in ``paper_2508_17522_b200/_lib/`` so it travels
 with the repository snapshot to the GPU box.
 """
 
+import hashlib
 import os
 import shutil
 import subprocess
@@ -45,8 +46,20 @@ def build(verbose=False, force=False, out=None, defines=()):
     ``defines`` (e.g. ``["QG_PSD_DMMA=0"]``) builds an A/B variant of the
     compile-time switches; load it with ``QG_LIB_PATH``.
     """
+    default_out = out is None or os.path.abspath(out) == os.path.abspath(globals()["OUT"])
+    if defines and default_out:
+        raise ValueError("variant builds (defines) must go to their own --out directory, not the production _lib/")
     OUT = out or globals()["OUT"]
     os.makedirs(OUT, exist_ok=True)
+    # objects compiled with other flags / defines are never reused: the stamp
+    # holds a hash of the compile line; a mismatch forces a full rebuild
+    stamp = os.path.join(OUT, ".build_stamp")
+    want = hashlib.sha256("\0".join(NVCC_FLAGS + sorted(defines)).encode()).hexdigest()
+    try:
+        with open(stamp) as f:
+            force = force or f.read().strip() != want
+    except OSError:
+        force = True
     headers = [os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "qcpgrad.h"))
     objs = []
@@ -72,6 +85,8 @@ def build(verbose=False, force=False, out=None, defines=()):
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
+    with open(stamp, "w") as f:
+        f.write(want)
     return lib
 
 

@@ -16,6 +16,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "operator.h"
 
@@ -72,7 +73,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(rk1); dev_free(done);
+  dev_free(st); dev_free(d_nactive); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -83,16 +84,19 @@ struct GraphCache {
     for (auto &kv : graph) cudaGraphDestroy(kv.second);
   }
 };
-// One executable graph per (jvp, iters) shared by all handles: switching
-// handles re-points its kernel nodes with cudaGraphExecUpdate (same topology,
-// new arguments / grid sizes) instead of re-instantiating -- a new batch per
-// training step pays one capture, not an instantiation.
+// One executable graph per (stream, jvp, iters) shared by all handles used
+// on that stream: switching handles re-points its kernel nodes with
+// cudaGraphExecUpdate (same topology, new arguments / grid sizes) instead of
+// re-instantiating -- a new batch per training step pays one capture, not an
+// instantiation.  Launches of one exec are serialised by CUDA, so keying by
+// stream keeps independent streams (host threads) concurrent.
 struct SharedExec {
   cudaGraphExec_t exec = nullptr;
   const Handle *owner = nullptr;
 };
+using ExecKey = std::tuple<cudaStream_t, int, int>;
 static std::map<const Handle *, GraphCache *> g_graphs;
-static std::map<std::pair<int, int>, SharedExec> g_exec;
+static std::map<ExecKey, SharedExec> g_exec;
 static std::mutex g_graph_mu;
 
 Handle::~Handle() {
@@ -133,6 +137,7 @@ struct Tracer {
 };
 
 static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
+  NvtxRange nv("qg:prepare");
   Tracer trace(st);
   const int B = (int)d.nprob;
   if (B <= 0) throw Error{QG_ERR_VALIDATION, "batch must hold at least one problem"};
@@ -255,8 +260,6 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.part = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
-  W.done = dev_alloc<int>(B);
-  QG_CUDA(cudaMemsetAsync(W.done, 0, sizeof(int) * B, st));
   W.h_nactive = nullptr;
   if (H.comm) {
     H.xred = dev_alloc<double>(H.NX);
@@ -315,35 +318,8 @@ static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &
   fv.rk1 = rk1;
 }
 
-// Fused finalize (the last CTA of each problem runs k_fin's work at the end
-// of the step; 2 instead of 4 launches per iteration): whole-problem handles
-// without rank-one term or staging, opt-in with QG_FUSED_FIN=1.  Measured per
-// jvp+vjp step (separate -> fused): c1 7.62 -> 7.82 ms, c2 12.9 -> 14.2, c3
-// 26.2 -> 26.6, c4 52.4 -> 53.1, c5b 139.5 -> 131.3, c5a 267 -> 300: the
-// serial finalize tail of the last CTA costs more than the launch it saves.
-static bool fused_fin_ok(const Handle &H) {
-  static const char *env = std::getenv("QG_FUSED_FIN");
-  if (!env || !std::atoi(env)) return false;
-  return !H.comm && !H.use_rk1;
-}
-
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
   const int ku = jvp ? STEP_F : STEP_FT, kv = jvp ? STEP_FT : STEP_F;
-  if (fused_fin_ok(H)) {  // 2 launches / iteration
-    StepArgs su, sv;
-    FinArgs fu, fv;
-    iter_args(H, jvp, su, sv, fu, fv);
-    fin_ptrs(H, fu);
-    fin_ptrs(H, fv);
-    su.done = sv.done = H.ws.done;
-    su.fin = fu;
-    sv.fin = fv;
-    for (int i = 0; i < iters; ++i) {
-      launch_step(H, M, ku, su, st);
-      launch_step(H, M, kv, sv, st);
-    }
-    return;
-  }
   // The vector update of iteration k (hbar, x, h) runs fused into the u-step
   // kernel of iteration k+1 (which streams v_k anyway), and its stopping
   // test runs at the head of that iteration's PH_STEP_U finalize; the last
@@ -403,7 +379,7 @@ static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStre
   GraphCache *gc = git->second;
   auto cit = gc->graph.find(key);
   if (cit == gc->graph.end()) cit = gc->graph.emplace(key, capture_graph(H, M, jvp, iters)).first;
-  SharedExec &se = g_exec[key];
+  SharedExec &se = g_exec[ExecKey{st, key.first, key.second}];
   if (se.exec == nullptr) {
     QG_CUDA(cudaGraphInstantiate(&se.exec, cit->second, 0));
   } else if (se.owner != &H) {
@@ -432,23 +408,12 @@ static int kernels_per_iter(const Handle &H) {
   // row-partitioned: each step is X_PARTIAL + X_FINISH and each finalize is
   // k_part_reduce + k_fin (the NCCL kernels are not ours)
   if (H.comm) return 8 - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
-  if (fused_fin_ok(H)) return H.nxu() + H.nyu() == 0 ? 0 : 2;
   return 4 - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
   Workspace &W = H.ws;
-  if (resident_ok(H)) {
-    // one launch: each CTA runs whole problems to their stopping rule (the
-    // per-problem caps live in the LSMR state), no host polling
-    StepArgs su, sv;
-    FinArgs fu, fv;
-    iter_args(H, jvp, su, sv, fu, fv);
-    launch_lsmr_resident(H, M, jvp ? STEP_F : STEP_FT, su, sv, fu, fv, st);
-    return;
-  }
   long long done = 0;
-  const bool persistent = persistent_ok(H);
   while (true) {
     launch_count_active(H, st);
     int *pinned = pinned_word();
@@ -459,16 +424,8 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
     // 16 first (early convergence wastes little), then chunks of 64
     const long long want = done == 0 ? std::min<long long>(rem, 16) : rem;
     const int g = want >= 64 ? 64 : (want >= 16 ? 16 : (want >= 4 ? 4 : 1));
-    if (persistent) {
-      // one cooperative launch for all g iterations (counted as it launches)
-      StepArgs su, sv;
-      FinArgs fu, fv;
-      iter_args(H, jvp, su, sv, fu, fv);
-      launch_lsmr_persistent(H, M, jvp ? STEP_F : STEP_FT, su, sv, fu, fv, g, st);
-    } else {
-      launch_iters(H, M, jvp, g, st);
-      if (!H.comm || H.comm->capturable()) count_launch(g * kernels_per_iter(H));  // else counted as launched
-    }
+    launch_iters(H, M, jvp, g, st);
+    if (!H.comm || H.comm->capturable()) count_launch(g * kernels_per_iter(H));  // else counted as launched
     done += g;
   }
 }
@@ -517,6 +474,7 @@ static void lsmr_finish(Handle &H, qg_diag *diag, cudaStream_t st) {
 // After the rhs is in W.u (and, for vjp, D Pi(u_Y) in W.dpu): initial
 // v = OP'(u)/beta, alpha, h = v, hbar = x = 0 (lsmr.py:72-103), then loop.
 static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long long cap, cudaStream_t st) {
+  NvtxRange nv(jvp ? "qg:lsmr(F)" : "qg:lsmr(F')");
   Workspace &W = H.ws;
   FinArgs fr{H.B, PH_RHS, rhs_kind, W.st, W.part, W.u, nullptr, W.u, W.h, W.hb, W.x, W.v};
   launch_fin(H, M, fr, st);
@@ -561,6 +519,7 @@ static int create_batch(qg_handle **out, const qg_batch_desc *desc, qg_comm *com
   try {
     build_handle(*H, *desc, st);
     launch_sub(H->ybar, H->cones.d_zmid, H->sbar, H->NY, st);
+    // host fence before any PDL chain (operator.cu, launch_pdl invariant)
     QG_CUDA(cudaStreamSynchronize(st));
   } catch (...) {
     delete H;
@@ -668,6 +627,8 @@ static void set_point(Handle &H, const double *z, bool want_deriv, cudaStream_t 
   Mats M = make_mats(H);
   launch_embed_consts(H, M, H.ws.part, st, z + H.NX + H.NY);
   launch_sub(H.ybar, zmid, H.sbar, H.NY, st);
+  // host fence: emb and the D Pi data are read before griddepcontrol.wait by
+  // the PDL-launched step kernels (operator.cu, launch_pdl invariant)
   QG_CUDA(cudaStreamSynchronize(st));
   H.normalized = norm;
   H.deriv_ready = want_deriv;
@@ -708,10 +669,14 @@ int qg_jvp(qg_handle *h, const qg_perturbation *d, const qg_lsmr_opts *opts, dou
   try {
     long long cap;
     lsmr_begin(H, *opts, st, cap);
-    launch_jvp_rhs(H, M, pd, W.u, W.part, st);
+    {
+      NvtxRange nv("qg:jvp rhs");
+      launch_jvp_rhs(H, M, pd, W.u, W.part, st);
+    }
     lsmr_solve(H, M, true, RHS_JVP, cap, st);
     lsmr_finish(H, diag, st);
     // D phi: dy/ds need D Pi(dz_mid)
+    NvtxRange nv("qg:jvp assembly");
     H.cones.apply(W.x + H.NX, W.tY, st);
     launch_dphi(H, M, W.x, W.tY, dx, dy, ds, st);
     QG_CUDA(cudaStreamSynchronize(st));
@@ -735,12 +700,16 @@ int qg_vjp(qg_handle *h, const double *dx, const double *dy, const double *ds, c
   long long cap;
   lsmr_begin(H, *opts, st, cap);
   // dz = D phi'(delta): D Pi(dy + ds) - ds ; rhs = -dz ; D Pi(rhs_Y) for the first F
-  launch_add(H, dy, ds, W.tY2, H.NY, st);
-  H.cones.apply(W.tY2, W.tY, st);
-  launch_vjp_rhs(H, M, dx, dy, ds, W.tY, W.u, W.part, st);
-  H.cones.apply(W.u + H.NX, W.dpu, st);
+  {
+    NvtxRange nv("qg:vjp rhs");
+    launch_add(H, dy, ds, W.tY2, H.NY, st);
+    H.cones.apply(W.tY2, W.tY, st);
+    launch_vjp_rhs(H, M, dx, dy, ds, W.tY, W.u, W.part, st);
+    H.cones.apply(W.u + H.NX, W.dpu, st);
+  }
   lsmr_solve(H, M, false, RHS_VJP, cap, st);
   lsmr_finish(H, diag, st);
+  NvtxRange nv("qg:vjp assembly");
   launch_vjp_grad(H, M, W.x, dP_vals, dA_vals, dq, db, st);
   QG_CUDA(cudaStreamSynchronize(st));
   QG_API_END

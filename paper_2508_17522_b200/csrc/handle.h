@@ -50,9 +50,8 @@ struct SellMat {
   int32_t *w = nullptr;
   int32_t *col = nullptr;
   double *val = nullptr;
-  uint16_t *col16 = nullptr;
   int64_t entries = 0;
-  SellView view() const { return SellView{off, w, col, val, col16}; }
+  SellView view() const { return SellView{off, w, col, val}; }
   void release();
 };
 
@@ -63,7 +62,6 @@ struct Workspace {
   double *rk1 = nullptr;     // EVec: refine rank-one vector (allocated on first use)
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
-  int *done = nullptr;       // [B] per-problem arrival counters of the fused finalize (kept 0)
   int *h_nactive = nullptr;  // pinned
   void release();
 };

@@ -11,13 +11,9 @@
 //   k_fin       stopping rules                                     (lsmr.py:173-182)
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
-#include <cooperative_groups.h>
-
 #include "dpi_dev.cuh"
 #include "ops_dev.cuh"
 #include "operator.h"
-
-namespace cg = cooperative_groups;
 
 namespace qg {
 
@@ -59,9 +55,6 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 #ifndef QG_SLICE_CLAIM
 #define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
 #endif
-#ifndef QG_META_PREFETCH
-#define QG_META_PREFETCH 0  // 1: load the next slice pair's metadata during the current pair (A/B)
-#endif
 template <bool WIDE, int UNR, int ROWS32, int ROWSG, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
@@ -74,43 +67,6 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     __shared__ int next_slice;
     if (threadIdx.x == 0) next_slice = u.s0;
     __syncthreads();
-#if QG_META_PREFETCH
-    // the next pair is claimed and its metadata (offsets, widths, row map)
-    // loaded while the current pair streams
-    auto claim = [&]() {
-      int s = 0;
-      if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
-      return __shfl_sync(0xffffffffu, s, 0);
-    };
-    struct Pair {
-      SliceMeta m1, m2;
-      int ra, rb;
-    };
-    auto fetch = [&](int s) {
-      Pair q{};
-      const int sb = (QG_SLICE_CLAIM == 2 && s + 1 < u.s1) ? s + 1 : -1;
-      q.m1 = slice_meta(S1, s, sb, lane);
-      if (S2) q.m2 = slice_meta(*S2, s, sb, lane);
-      q.ra = rowof[(int64_t)s * 32 + lane];
-      q.rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
-      return q;
-    };
-    int s = claim();
-    Pair cur{};
-    if (s < u.s1) cur = fetch(s);
-    while (s < u.s1) {
-      const int sn = claim();
-      Pair nxt{};
-      if (sn < u.s1) nxt = fetch(sn);
-      double a1, b1v, a2 = 0.0, b2v = 0.0;
-      sell_dot2<UNR>(S1, cur.m1, x1, x1 + b1, a1, b1v);
-      if (S2) sell_dot2<UNR>(*S2, cur.m2, x2, x2 + b2, a2, b2v);
-      if (cur.ra >= 0) row(cur.ra, a1, a2);
-      if (cur.rb >= 0) row(cur.rb, b1v, b2v);
-      s = sn;
-      cur = nxt;
-    }
-#else
     while (true) {
       int s = 0;
       if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
@@ -120,12 +76,11 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
       double a1, b1v, a2 = 0.0, b2v = 0.0;
-      sell_dot2<UNR>(S1, s, sb, lane, x1, x1 + b1, a1, b1v);
-      if (S2) sell_dot2<UNR>(*S2, s, sb, lane, x2, x2 + b2, a2, b2v);
+      sell_dot2<UNR>(S1, s, sb, lane, x1, a1, b1v);
+      if (S2) sell_dot2<UNR>(*S2, s, sb, lane, x2, a2, b2v);
       if (ra >= 0) row(ra, a1, a2);
       if (rb >= 0) row(rb, b1v, b2v);
     }
-#endif
   } else if (WIDE && u.mode == MODE_WIDE) {
     // the whole CTA per CSR row: 4 independent partial sums per thread keep
     // the loads in flight, then a fixed-order warp / CTA reduction
@@ -205,16 +160,16 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
           for (int j = 0; j < R; ++j)
             if (r + j * stride < u.row1) row(r + j * stride, s1[j], s2[j]);
       }
-      return;
-    }
-    for (int base = u.row0 + warp * gpw; base < u.row1; base += nw * gpw) {
-      const int r = base + lane / G;
-      const bool valid = r < u.row1;
-      double s1 = valid ? row_dot(rp1, c1, v1, x1, r, lg, G) : 0.0;
-      double s2 = (valid && rp2) ? row_dot(rp2, c2, v2, x2, r, lg, G) : 0.0;
-      s1 = gsum(s1, G);
-      s2 = gsum(s2, G);
-      if (valid && lg == 0) row(r, s1, s2);
+    } else {
+      for (int base = u.row0 + warp * gpw; base < u.row1; base += nw * gpw) {
+        const int r = base + lane / G;
+        const bool valid = r < u.row1;
+        double s1 = valid ? row_dot(rp1, c1, v1, x1, r, lg, G) : 0.0;
+        double s2 = (valid && rp2) ? row_dot(rp2, c2, v2, x2, r, lg, G) : 0.0;
+        s1 = gsum(s1, G);
+        s2 = gsum(s2, G);
+        if (valid && lg == 0) row(r, s1, s2);
+      }
     }
   }
 }
@@ -270,25 +225,18 @@ constexpr int kStepThreads = 128;
 #ifndef QG_PSD_PREFETCH
 #define QG_PSD_PREFETCH 1
 #endif
-#ifndef QG_RESIDENT_MINB
-#define QG_RESIDENT_MINB 8
-#endif
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatFin = 16;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
-
-__device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
-                                            const double *pre = nullptr, Lsmr *Lsh = nullptr);
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
-// a.rk1 is set), kFeatFin (fused finalize).
+// a.rk1 is set).
 // The common variant (0) carries none of them.
 // One work unit (`ui`: X units then Y units) of an operator step, by the
 // whole CTA; the partial-sum slot of the unit is part[ui].
 template <int KIND, int FEAT, bool SELL8 = false>
 __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int ui) {
   constexpr bool kDist = (FEAT & kFeatDist) != 0, kWide = (FEAT & kFeatWide) != 0;
-  constexpr bool kFin = (FEAT & kFeatFin) != 0;
   constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;  // SELL entry-loop unroll
   // rows per warp, warp-per-row CSR; SELL8 = the 8-CTA/SM SELL F instantiation
   constexpr int kRows32 = KIND == STEP_F ? (SELL8 ? QG_ROWS32_SELL : QG_ROWS32) : QG_ROWS32_FT;
@@ -306,12 +254,6 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   const double wN = a.in[M.NX + M.NY + p];             // issued with the LSMR-state loads below
   double s_in, c_out;
   if (!lsmr_runs(a, p, s_in, c_out)) {  // CTA-uniform
-    // a skipped v-step (beta = 0) still runs its finalize recurrences
-    // (k_fin PH_STEP_V): the problem's first unit does it, no partials needed
-    if (kFin && a.is_v_step && a.st[p].active && a.st[p].skip_v && threadIdx.x < 32) {
-      const int first = M.xu_ptr[p] < M.xu_ptr[p + 1] ? (int)M.xu_ptr[p] : M.nxu + (int)M.yu_ptr[p];
-      if (ui == first) fin_problem(M, a.fin, p, (int)threadIdx.x);
-    }
     if (KIND == STEP_FT && QG_PSD_PREFETCH) asm volatile("cp.async.wait_all;" ::: "memory");  // (prefetch)
     return;
   }
@@ -449,23 +391,6 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   if (threadIdx.x == 0 && a.part)
 #pragma unroll
     for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
-  if (kFin) {
-    // last CTA of problem p to finish runs its finalize (threadFenceReduction
-    // pattern); the slot sums stay in k_fin's fixed order
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-      __threadfence();
-      const int total = (int)(M.xu_ptr[p + 1] - M.xu_ptr[p] + M.yu_ptr[p + 1] - M.yu_ptr[p]);
-      const int prev = atomicAdd(a.done + p, 1);
-      s_last = prev == total - 1;
-      if (s_last) a.done[p] = 0;  // every unit of p has arrived: reset for the next step
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x < 32) {
-      __threadfence();
-      fin_problem(M, a.fin, p, (int)threadIdx.x);
-    }
-  }
 }
 
 template <int KIND, int MINB, int FEAT>
@@ -592,9 +517,7 @@ __device__ __forceinline__ bool fin_skips(const FinArgs &a, int p) {
 // shared-memory copy of the problem's LSMR state to work on (the caller
 // loads and stores it cooperatively), else the state in global memory.
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
-                                            const double *pre, Lsmr *Lsh) {
-  // partials are read L2-coherent (__ldcg): in the fused variant they were
-  // written by other CTAs of the same launch
+                                            const double *pre = nullptr, Lsmr *Lsh = nullptr) {
   Lsmr *L = Lsh ? Lsh : (a.st ? a.st + p : nullptr);
   if (fin_skips(a, p)) return;
   // deterministic per-problem sums of the producers' partials (fixed order)
@@ -846,82 +769,6 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
   }
 }
 
-// Persistent LSMR for small batches (launch latency, not bandwidth, bounds
-// them): ONE cooperative launch runs `iters` iterations -- u-step over all
-// units, grid barrier, finalize (one warp per problem), barrier, v-step,
-// barrier, finalize, barrier -- the same device code as the 4-launch
-// graph path, so the arithmetic (and the results) are identical.
-struct LoopArgs {
-  StepArgs su, sv;
-  FinArgs fu, fv;
-  int iters;
-};
-
-template <int KU, int KV>
-__global__ void __launch_bounds__(kStepThreads, 4) k_lsmr_loop(Mats M, LoopArgs L) {
-  cg::grid_group grid = cg::this_grid();
-  const int nunits = M.nxu + M.nyu;
-  const int lane = threadIdx.x & 31;
-  const int gw = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-  const int nw = (int)(((int64_t)gridDim.x * blockDim.x) >> 5);
-  for (int it = 0; it < L.iters; ++it) {
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      step_unit<KU, 0>(M, L.su, u);
-      __syncthreads();
-    }
-    grid.sync();
-    for (int p = gw; p < L.fu.B; p += nw) fin_problem(M, L.fu, p, lane);
-    grid.sync();
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-      step_unit<KV, 0>(M, L.sv, u);
-      __syncthreads();
-    }
-    grid.sync();
-    for (int p = gw; p < L.fv.B; p += nw) fin_problem(M, L.fv, p, lane);
-    grid.sync();
-  }
-}
-
-// Problem-resident LSMR (large batches of small problems, c5a): each CTA
-// claims a whole problem and runs ALL of its remaining iterations -- u-step
-// over the problem's units, finalize (warp 0), v-step, finalize -- with only
-// CTA barriers in between, then claims the next problem.  Same device code
-// and per-unit partial-sum order as the graph path (identical results); no
-// kernel boundaries, no grid-wide tails, the problem's vectors stay hot in
-// the SM's L1 for the whole solve, and a converged problem frees its CTA at
-// once.  `next` is the claim counter (zeroed by the caller).
-template <int KU, int KV, int FEAT>
-__device__ __forceinline__ void resident_body(const Mats &M, const LoopArgs &L, int *next) {
-  __shared__ int s_p, s_go;
-  const int lane = threadIdx.x & 31;
-  while (true) {
-    if (threadIdx.x == 0) s_p = atomicAdd(next, 1);
-    __syncthreads();
-    const int p = s_p;
-    if (p >= L.fu.B) return;
-    const int x0 = (int)M.xu_ptr[p], x1 = (int)M.xu_ptr[p + 1];
-    const int y0 = M.nxu + (int)M.yu_ptr[p], y1 = M.nxu + (int)M.yu_ptr[p + 1];
-    while (true) {
-      if (threadIdx.x == 0) s_go = L.fu.st[p].active;
-      __syncthreads();
-      if (!s_go) break;
-      for (int u = x0; u < x1; ++u) { step_unit<KU, FEAT>(M, L.su, u); __syncthreads(); }
-      for (int u = y0; u < y1; ++u) { step_unit<KU, FEAT>(M, L.su, u); __syncthreads(); }
-      if (threadIdx.x < 32) fin_problem(M, L.fu, p, lane);   // stop test of the previous iteration first
-      __syncthreads();
-      for (int u = x0; u < x1; ++u) { step_unit<KV, FEAT>(M, L.sv, u); __syncthreads(); }
-      for (int u = y0; u < y1; ++u) { step_unit<KV, FEAT>(M, L.sv, u); __syncthreads(); }
-      if (threadIdx.x < 32) fin_problem(M, L.fv, p, lane);
-      __syncthreads();
-    }
-  }
-}
-
-template <int KU, int KV, int FEAT>
-__global__ void __launch_bounds__(kStepThreads, QG_RESIDENT_MINB) k_lsmr_resident(Mats M, LoopArgs L, int *next) {
-  resident_body<KU, KV, FEAT>(M, L, next);
-}
-
 // (Measured and dropped: the same loop as ONE 1024-thread CTA for a single
 // tiny problem with whole-problem units -- c1 8.1 -> 9.5 ms per step.)
 
@@ -971,6 +818,16 @@ static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cone
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger
 // in qg_common.cuh); QG_PDL=0 falls back to ordinary serialization (A/B).
+//
+// INVARIANT (pre-wait reads): k_step reads preparation-time data -- the
+// work units, M.emb and (cp.async) the PSD eigenvectors V -- BEFORE its
+// griddepcontrol.wait, so those reads may overlap the previous kernel.  This
+// is only correct because every writer of that data (k_embed_* in
+// launch_embed_consts, k_cone_prep in ConeTable::prepare, the unit / SELL
+// uploads) runs in qg_create_batch* or qg_set_point, and both end with a
+// cudaStreamSynchronize before any PDL chain (a jvp / vjp / apply_F) starts.
+// A new writer of emb / D Pi data must keep that host fence (or launch a
+// non-PDL kernel between it and the first step launch).
 template <class... KArgs, class... Args>
 static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args &&...args) {
@@ -1032,20 +889,18 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   };
   // the CTA-per-row path and the rarely used features run as their own
   // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
-  // partitioned / rank-one steps the all-features one.  The fused finalize
-  // (a.done set by the loop driver) has its own plain / wide variants.
+  // partitioned / rank-one steps the all-features one
   const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
-  const bool fin = a.done != nullptr && feat != kFeatAll;
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
-    else if (feat == kFeatWide) fin ? go(k_step<STEP_F, 12, kFeatWide | kFeatFin>, 0) : go(k_step<STEP_F, 12, kFeatWide>, 0);
-    else if (minb == 12) fin ? go(k_step<STEP_F, 12, kFeatFin>, 0) : go(k_step<STEP_F, 12, 0>, 0);
-    else fin ? go(k_step<STEP_F, 8, kFeatFin>, 0) : go(k_step<STEP_F, 8, 0>, 0);
+    else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
+    else if (minb == 12) go(k_step<STEP_F, 12, 0>, 0);
+    else go(k_step<STEP_F, 8, 0>, 0);
   } else {
     if (feat == kFeatAll) go(k_step<STEP_FT, 12, kFeatAll>, smem);
-    else if (feat == kFeatWide) fin ? go(k_step<STEP_FT, 12, kFeatWide | kFeatFin>, smem) : go(k_step<STEP_FT, 12, kFeatWide>, smem);
-    else if (minb == 12) fin ? go(k_step<STEP_FT, 12, kFeatFin>, smem) : go(k_step<STEP_FT, 12, 0>, smem);
-    else fin ? go(k_step<STEP_FT, 8, kFeatFin>, smem) : go(k_step<STEP_FT, 8, 0>, smem);
+    else if (feat == kFeatWide) go(k_step<STEP_FT, 12, kFeatWide>, smem);
+    else if (minb == 12) go(k_step<STEP_FT, 12, 0>, smem);
+    else go(k_step<STEP_FT, 8, 0>, smem);
   }
   QG_LAUNCHED();
 }
@@ -1078,84 +933,6 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
   const bool cta = !H.comm && (env ? std::atoi(env) != 0 : (int64_t)(H.nxu() + H.nyu()) >= 64LL * H.B);
   if (cta) launch_pdl(k_fin_cta, dim3((unsigned)H.B), dim3(256), 0, st, M, a);
   else launch_pdl(k_fin, dim3(grid), dim3(256), 0, st, M, a);
-  QG_LAUNCHED();
-}
-
-// The persistent loop applies to plain whole-problem handles (no row
-// partition, rank-one term, CTA-per-row units or staging) and is opt-in
-// (QG_PERSIST=1).  Measured per jvp+vjp step at K=100 (graph path -> persistent):
-// c1 7.8 -> 11.4 ms, c2 11.1 -> 20.2, c3 23.2 -> 43.7, c4 50.6 -> 47.1.  The
-// small configs are bound by each step's own dependent-load latency, not by
-// launches, and four grid barriers per iteration cost more than four graph
-// kernel nodes.
-bool persistent_ok(const Handle &H) {
-  if (H.comm || H.use_rk1 || H.has_wide) return false;
-  static const char *env = std::getenv("QG_PERSIST");
-  return env && std::atoi(env) != 0;
-}
-
-// Problem-resident loop: whole-problem handles (no row partition, no
-// rank-one term); opt-in with QG_RESIDENT=1.  Measured on c5a (fixed K=100):
-// 376 ms per step vs 261 ms for the 4-launch graph path -- the graph path
-// runs a problem's units concurrently on different SMs, while here they run
-// back to back in one CTA (with 440 B of register spills at 64 registers).
-bool resident_ok(const Handle &H) {
-  if (H.comm || H.use_rk1) return false;
-  static const char *env = std::getenv("QG_RESIDENT");
-  return env && std::atoi(env) != 0;
-}
-
-void launch_lsmr_resident(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
-                          const FinArgs &fu0, const FinArgs &fv0, cudaStream_t st) {
-  LoopArgs L{su, sv, fu0, fv0, 0};
-  fin_ptrs(H, L.fu);
-  fin_ptrs(H, L.fv);
-  const size_t smem = step_smem(H);
-  const int threads = kStepThreads;
-  void *kern;
-  if (H.has_wide)
-    kern = ku == STEP_F ? (void *)k_lsmr_resident<STEP_F, STEP_FT, kFeatWide>
-                        : (void *)k_lsmr_resident<STEP_FT, STEP_F, kFeatWide>;
-  else
-    kern = ku == STEP_F ? (void *)k_lsmr_resident<STEP_F, STEP_FT, 0> : (void *)k_lsmr_resident<STEP_FT, STEP_F, 0>;
-  if (smem > 48 * 1024)
-    QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
-  QG_CUDA(cudaGetDevice(&dev));
-  QG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  QG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(H.B, (int64_t)std::max(per_sm, 1) * sms));
-  int *next = H.ws.d_nactive;  // reused as the claim counter
-  QG_CUDA(cudaMemsetAsync(next, 0, sizeof(int), st));
-  Mats m = M;
-  void *args[] = {&m, &L, &next};
-  QG_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(threads), args, smem, st));
-  QG_LAUNCHED();
-}
-
-void launch_lsmr_persistent(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
-                            const FinArgs &fu0, const FinArgs &fv0, int iters, cudaStream_t st) {
-  LoopArgs L{su, sv, fu0, fv0, iters};
-  for (FinArgs *f : {&L.fu, &L.fv}) {
-    f->px = H.ws.part;
-    f->px_ptr = H.d_xunit_ptr;
-    f->py = H.ws.part + (size_t)H.nxu() * kSlots;
-    f->py_ptr = H.d_yunit_ptr;
-  }
-  const size_t smem = step_smem(H);
-  void *kern = ku == STEP_F ? (void *)k_lsmr_loop<STEP_F, STEP_FT> : (void *)k_lsmr_loop<STEP_FT, STEP_F>;
-  if (smem > 48 * 1024)
-    QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
-  QG_CUDA(cudaGetDevice(&dev));
-  QG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  QG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStepThreads, smem));
-  if (per_sm < 1) throw Error{QG_ERR_CUDA, "persistent LSMR kernel does not fit an SM"};
-  const int64_t want = std::max<int64_t>(std::max<int64_t>(H.nxu() + H.nyu(), (H.B + 3) / 4), 1);
-  const unsigned grid = (unsigned)std::min<int64_t>(want, (int64_t)per_sm * sms);
-  Mats m = M;
-  void *args[] = {&m, &L};
-  QG_CUDA(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(kStepThreads), args, smem, st));
   QG_LAUNCHED();
 }
 

@@ -47,11 +47,6 @@ struct StepArgs {
   // rank-one term of the refine Jacobian J = F - r e_N' (testkit.py:443-451):
   // F step out -= r w_N ; F' step T out -= r'w (dot partial in slot 3)
   const double *rk1 = nullptr;
-  // fused finalize: the last CTA of each problem (per-problem arrival counter
-  // `done`) runs that problem's finalize `fin` at the end of the step --
-  // 2 instead of 4 dependent launches per LSMR iteration
-  int *done = nullptr;
-  FinArgs fin{};
 };
 
 struct UpdArgs {
@@ -66,16 +61,6 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cu
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
 void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole-problem handle
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
-// Persistent cooperative LSMR loop (small batches): eligibility, and one
-// launch running `iters` iterations with the given step / finalize arguments.
-bool persistent_ok(const Handle &H);
-// Problem-resident loop (one CTA runs a whole problem's iterations; batches
-// of many small problems): eligibility and the single launch.
-bool resident_ok(const Handle &H);
-void launch_lsmr_resident(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
-                          const FinArgs &fu, const FinArgs &fv, cudaStream_t st);
-void launch_lsmr_persistent(const Handle &H, const Mats &M, int ku, const StepArgs &su, const StepArgs &sv,
-                            const FinArgs &fu, const FinArgs &fv, int iters, cudaStream_t st);
 void launch_count_active(const Handle &H, cudaStream_t st);
 void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st);
 

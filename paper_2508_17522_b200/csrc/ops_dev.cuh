@@ -33,27 +33,8 @@ enum XMode : int { X_FULL = 0, X_PARTIAL = 1, X_FINISH = 2 };
 // Streamed matrix loads (each stored entry is read once per step):
 // read-only and not allocated in L1, so the gathered vectors keep the L1 to
 // themselves (c5a: F 0.462 -> 0.454 ms, F' 0.584 -> 0.574 ms vs __ldcs).
-#ifndef QG_L2_EVICT_FIRST
-#define QG_L2_EVICT_FIRST 0  // 1: also mark the streamed entries evict-first in L2 (A/B)
-#endif
-#ifndef QG_LDCS_LOADS
-#if QG_L2_EVICT_FIRST
-__device__ __forceinline__ unsigned long long l2_evict_first() {
-  unsigned long long pol;  // uniform; ptxas keeps it in the load's descriptor
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ double ld_stream(const double *p) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
-  return v;
-}
-__device__ __forceinline__ int ld_stream(const int *p) {
-  int v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first()));
-  return v;
-}
-#else
+// (Measured and dropped: an L2 evict-first policy on these loads, within
+// 0.3% on c5a, c5b and c3.)
 __device__ __forceinline__ double ld_stream(const double *p) {
   double v;
   asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
@@ -64,12 +45,6 @@ __device__ __forceinline__ int ld_stream(const int *p) {
   asm("ld.global.nc.L1::no_allocate.s32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
-#endif
-__device__ __forceinline__ unsigned short ld_stream(const unsigned short *p) { return __ldcs(p); }
-#else
-template <class T>
-__device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
-#endif
 
 // Two slices of one matrix at once (independent load streams -> twice the
 // memory-level parallelism per warp); slice b may be absent (sb < 0).  Each
@@ -77,59 +52,15 @@ __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
 // UNR: unroll of the entry loop.  Measured on c5a (ms, F / F'): 2 -> 0.520 /
 // 0.527, 4 -> 0.454 / 0.574, 8 -> 0.563 / 0.588: the F step wants 4, the F'
 // step (which also carries the epilogue at 40 registers) wants 2.
-template <int UNR, class Idx>
-__device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *col, int64_t sa, int64_t sb, int lane,
-                                            const double *vec, double &acc_a, double &acc_b);
-
-// Dispatch on the index width: 16-bit problem-local indices gather from
-// vec_local (= vec + this problem's column base), 32-bit global ones from vec.
+// (Measured and dropped: 16-bit problem-local column indices -- the gathers
+// are latency-, not byte-bound, and the local base costs an add per entry.)
 template <int UNR>
 __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t sb, int lane, const double *vec,
-                                          const double *vec_local, double &acc_a, double &acc_b) {
-  if (S.col16) sell_dot2_t<UNR>(S, S.col16, sa, sb, lane, vec_local, acc_a, acc_b);
-  else sell_dot2_t<UNR>(S, S.col, sa, sb, lane, vec, acc_a, acc_b);
-}
-
-// Start offsets (this lane) and widths of a slice pair; b absent -> width 0.
-struct SliceMeta {
-  int64_t oa, ob;
-  int wa, wb;
-};
-
-__device__ __forceinline__ SliceMeta slice_meta(const SellView &S, int64_t sa, int64_t sb, int lane) {
-  SliceMeta m;
-  m.oa = S.off[sa] + lane;
-  m.wa = S.w[sa];
-  m.ob = sb >= 0 ? S.off[sb] + lane : 0;
-  m.wb = sb >= 0 ? S.w[sb] : 0;
-  return m;
-}
-
-template <int UNR, class Idx>
-__device__ __forceinline__ void sell_dot2_m(const SellView &S, const Idx *colp, const SliceMeta &m,
-                                            const double *vec, double &acc_a, double &acc_b);
-
-// With metadata loaded ahead (the caller prefetches the next pair's while
-// this one streams).
-template <int UNR>
-__device__ __forceinline__ void sell_dot2(const SellView &S, const SliceMeta &m, const double *vec,
-                                          const double *vec_local, double &acc_a, double &acc_b) {
-  if (S.col16) sell_dot2_m<UNR>(S, S.col16, m, vec_local, acc_a, acc_b);
-  else sell_dot2_m<UNR>(S, S.col, m, vec, acc_a, acc_b);
-}
-
-template <int UNR, class Idx>
-__device__ __forceinline__ void sell_dot2_t(const SellView &S, const Idx *colp, int64_t sa, int64_t sb, int lane,
-                                            const double *vec, double &acc_a, double &acc_b) {
-  sell_dot2_m<UNR>(S, colp, slice_meta(S, sa, sb, lane), vec, acc_a, acc_b);
-}
-
-template <int UNR, class Idx>
-__device__ __forceinline__ void sell_dot2_m(const SellView &S, const Idx *colp, const SliceMeta &m,
-                                            const double *vec, double &acc_a, double &acc_b) {
-  const int64_t oa = m.oa, ob = m.ob;
-  const int wa = m.wa, wb = m.wb;
+                                          double &acc_a, double &acc_b) {
+  const int64_t oa = S.off[sa] + lane, ob = sb >= 0 ? S.off[sb] + lane : 0;
+  const int wa = S.w[sa], wb = sb >= 0 ? S.w[sb] : 0;
   const int wm = wa < wb ? wa : wb;
+  const int32_t *colp = S.col;
   double a = 0.0, b = 0.0;
   int k = 0;
 #pragma unroll UNR

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -107,8 +108,6 @@ struct SellView {
   const int32_t *w;     // [nslices] slice width (longest row)
   const int32_t *col;   // padded entries: col 0, val 0 (global column index)
   const double *val;
-  const uint16_t *col16;  // problem-local column index (null unless every problem
-                          // has < 65536 columns): 10 instead of 12 B per entry
 };
 
 // ------------------------------------------------------------ host utils --
@@ -170,6 +169,15 @@ __device__ __forceinline__ void cta_sum_slots(double (&v)[kSlots], double *smem_
   }
   __syncthreads();
 }
+
+// NVTX range for the phases of an API call (preparation, LSMR solve,
+// assembly); visible in nsys / ncu --nvtx.  Header-only NVTX v3.
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // Stream-ordered allocation from the device's default memory pool (kept
 // resident between handles: no cudaMalloc/cudaFree synchronisation on the

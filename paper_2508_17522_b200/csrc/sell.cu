@@ -25,8 +25,6 @@ void SellMat::release() {
   dev_free(w);
   dev_free(col);
   dev_free(val);
-  dev_free(col16);
-  col16 = nullptr;
   off = nullptr;
   w = nullptr;
   col = nullptr;
@@ -80,10 +78,9 @@ __global__ void k_width32(const int32_t *w, int64_t n, int64_t *out) {
 }
 
 // warp per slice: scatter the CSR rows into the slice layout
-// col16 (when non-null) receives col - cbase[slice] (problem-local index).
 __global__ void k_sell_fill(int64_t nslices, const int32_t *rowof, const int32_t *rp, const int32_t *csr_col,
                             const double *csr_val, const int64_t *off, const int32_t *w, int32_t *col, double *val,
-                            uint16_t *col16, const int32_t *cbase) {
+                            const int32_t *cbase) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;
@@ -98,15 +95,14 @@ __global__ void k_sell_fill(int64_t nslices, const int32_t *rowof, const int32_t
     const int64_t pos = o + 32LL * k + lane;
     const bool in = k < len;
     val[pos] = in ? csr_val[k0 + k] : 0.0;
-    if (col16) col16[pos] = in ? (uint16_t)(csr_col[k0 + k] - base) : (uint16_t)0;
-    else col[pos] = in ? csr_col[k0 + k] : base;
+    col[pos] = in ? csr_col[k0 + k] : base;
   }
 }
 
 inline unsigned nb(int64_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
 void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_t *wsrc, const DevCsr &csr,
-                 const int32_t *d_cbase, bool use16, cudaStream_t st) {
+                 const int32_t *d_cbase, cudaStream_t st) {
   M.w = dev_alloc<int32_t>(nslices);
   QG_CUDA(cudaMemcpyAsync(M.w, wsrc, sizeof(int32_t) * nslices, cudaMemcpyDeviceToDevice, st));
   int64_t *w32 = dev_alloc<int64_t>(nslices);
@@ -126,12 +122,11 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
   QG_CUDA(cudaMemcpyAsync(&total, M.off + nslices, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
   M.entries = total;
-  if (use16) M.col16 = dev_alloc<uint16_t>(total);
-  else M.col = dev_alloc<int32_t>(total);
+  M.col = dev_alloc<int32_t>(total);
   M.val = dev_alloc<double>(total);
   if (total > 0) {
     k_sell_fill<<<nb(nslices * 32), 256, 0, st>>>(nslices, rowof, csr.rp, csr.col, csr.val, M.off, M.w, M.col,
-                                                  M.val, M.col16, d_cbase);
+                                                  M.val, d_cbase);
     QG_LAUNCHED();
   }
   dev_free(tmp);
@@ -142,11 +137,11 @@ void fill_matrix(SellMat &M, int64_t nslices, const int32_t *rowof, const int32_
 // Decide modes and slice ranges on the host, sort rows on the device, build
 // the slice metadata and the padded matrices.  Returns the number of slices.
 // cb1 / cb2: per-problem column base of matrix 1 / 2 (X or Y offsets): the
-// padding column, and the subtrahend of the 16-bit local indices (use16).
+// padding column (a valid index of the problem's own vector).
 int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const int32_t *rp1, const int32_t *rp2,
                    const DevCsr &m1, const DevCsr *m2, SellMat &s1, SellMat *s2, int32_t **rowof_out,
                    bool allow_sell, const std::vector<int64_t> *cb1, const std::vector<int64_t> *cb2,
-                   bool use16, cudaStream_t st) {
+                   cudaStream_t st) {
   std::vector<int32_t> slice_pos, slice_n, slice_b1, slice_b2;
   int64_t ns = 0;
   const int max_row = allow_sell ? kSellMaxRow : -1;
@@ -229,8 +224,8 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
     QG_CUDA(cudaMemcpyAsync(d_b2, slice_b2.data(), sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
   }
   trace_point("  sell side: sort + slice meta", st);
-  fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, use16, st);
-  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, use16, st);
+  fill_matrix(s1, ns, *rowof_out, w1, m1, d_b1, st);
+  if (m2) fill_matrix(*s2, ns, *rowof_out, w2, *m2, d_b2, st);
   QG_CUDA(cudaStreamSynchronize(st));
   trace_point("  sell side: fill", st);
   dev_free(keys); dev_free(keys_s); dev_free(rows); dev_free(rows_s); dev_free(tmp);
@@ -253,16 +248,10 @@ void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_
   };
   const bool sx = sell_ok(H.NX, (int64_t)rpP[H.NX] + rpAT[H.NX]);
   const bool sy = sell_ok(H.NY, (int64_t)rpA[H.NY]);
-  // 16-bit problem-local column indices (every problem small enough): opt-in
-  // with QG_SELL16=1 -- measured slower than 32-bit on c5a (the gathers are
-  // latency-, not byte-bound; the local base costs an extra add per entry)
-  const char *f16 = std::getenv("QG_SELL16");
-  bool small = f16 ? std::atoi(f16) != 0 : false;
-  for (int p = 0; p < H.B && small; ++p) small = H.n[p] < 65536 && H.m[p] < 65536;
   H.nslice_x = build_side(H.xunits, H.d_xunits, H.NX, rpP, rpAT, H.P, &H.AT, H.sP, &H.sAT, &H.x_rowof, sx,
-                          &H.xoff, &H.yoff, small, st);
+                          &H.xoff, &H.yoff, st);
   H.nslice_y = build_side(H.cones.units, H.cones.d_units, H.NY, rpA, nullptr, H.A, nullptr, H.sA, nullptr,
-                          &H.y_rowof, sy, &H.xoff, nullptr, small, st);
+                          &H.y_rowof, sy, &H.xoff, nullptr, st);
   H.has_wide = false;
   for (const auto *us : {&H.xunits, &H.cones.units})
     for (const Unit &u : *us) H.has_wide = H.has_wide || u.mode == MODE_WIDE;

@@ -468,8 +468,13 @@ def _prepare(theta, sol, check, check_tol):
     q = QCP(theta, sol)
     report = None
     if check:
-        report = q.kkt(check_tol)
+        try:
+            report = q.kkt(check_tol)
+        except BaseException:
+            q.close()
+            raise
         if not report.ok:
+            q.close()  # release the handle's device buffers now, not at garbage collection
             exc = ValidationError("solution fails the optimality pre-check: "
                                   f"max violation {report.max_violation():.3e} > tolerance {report.tol:.3e} "
                                   "(pass check=False to differentiate anyway)")

@@ -1,5 +1,6 @@
 """GPU-vs-oracle vjp gap and the oracle's own operator-noise sensitivity
-(1e-16 relative noise on every F / F' output) across LSMR caps."""
+(1e-16 relative noise on every F / F' output) across LSMR caps:
+    python tools/cap_sensitivity.py c4 5 10 15 19 20"""
 import sys, os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT); sys.path.insert(0, os.path.join(ROOT, "tests"))
