@@ -16,6 +16,7 @@ relative; P2 jvp / vjp <= 1e-6 at matched caps, compared only at caps where
 the reference itself is stable under 1e-16 operator noise.
 """
 
+import re
 import threading
 
 import numpy as np
@@ -113,10 +114,17 @@ def test_c5a_forced_sell_small_batch(monkeypatch):
     monkeypatch.setenv("QG_SELL", "0")
     b0 = _batch(bt)
     assert b0.layout() == (0, 0)
+    # SELL vs CSR: the operator to ulp level (different summation trees) ...
+    w = _dev(np.random.default_rng(1).standard_normal(sum(bt.n) + sum(bt.m) + bt.B))
+    for t in (False, True):
+        assert gap(b.apply_F_device(w, transpose=t).cpu().numpy(),
+                   b0.apply_F_device(w, transpose=t).cpu().numpy()) <= 1e-13
+    # ... and fixed-cap jvp / vjp at the P2 bound (K=3 amplifies ulp
+    # differences to ~1e-8 here: the reference's own cap sensitivity)
     j1, v1 = _run(b, dirs, 3)
     j0, v0 = _run(b0, dirs, 3)
-    for a, c in zip(j1 + v1, j0 + v0):                                               # SELL vs CSR
-        assert gap(a, c) <= 1e-12
+    for a, c in zip(j1 + v1, j0 + v0):
+        assert gap(a, c) <= 1e-6
 
 
 @pytest.fixture(scope="module")
@@ -138,8 +146,17 @@ def test_c3_full_cones(c3):
     rng = np.random.default_rng(5)
     for z in (mid, mid * (1.0 + 1e-6 * rng.standard_normal(mid.size))):
         for dual in (True, False):
+            try:
+                want = C.project(th.blocks, z, dual=dual)
+            except C.BlockFailure as e:
+                # Pi_K (primal, off the path) of these points: the reference
+                # itself fails on block 2927 ("exponential cone projection
+                # root-finding did not converge", checked against conegrad
+                # 0.1.0) -- the GPU must fail the same way on the same block
+                with pytest.raises(qg.NumericalError, match=re.escape(str(e))):
+                    (qg.project_dual if dual else qg.project)(spec, z)
+                continue
             got = (qg.project_dual if dual else qg.project)(spec, z)
-            want = C.project(th.blocks, z, dual=dual)
             assert gap(got, want) <= 1e-12
         dz = rng.standard_normal(mid.size)
         got = qg.dprojection_dual(spec, z).matvec(dz)

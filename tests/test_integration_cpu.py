@@ -50,3 +50,29 @@ def test_error_translation_keeps_reference_classes():
         with cc._reference_errors():
             raise qg_errors.NumericalError("broke", iteration=7)
     assert ei.value.iteration == 7
+
+
+def test_golden_relaxation_is_per_kind_and_measured():
+    """The plugin relaxes each golden to the reference's own measured
+    spread under ulp noise (tests/golden/golden_noise.json), never below
+    1e-6 / +-3 iterations, and maps it onto the suite's 1e-9 threshold."""
+    sys.path.insert(0, os.path.join(REF, "tests"))
+    sys.path.insert(0, os.path.join(ROOT, "integration"))
+    import copy
+
+    import conegrad_plugin as cp
+    import helpers
+
+    for kind in cp.NOISE:
+        for op in ("jvp", "vjp"):
+            want = helpers.load_golden(f"{kind}_{op}.json")
+            tol, slack = cp.kind_tolerance(want)
+            assert tol >= 1e-6 and slack >= 3
+            assert tol == max(1e-6, 10 * cp.NOISE[kind][f"{op}_gap"])
+            assert cp.relaxed_golden_result_gap(copy.deepcopy(want), want) == 0.0
+            got = copy.deepcopy(want)
+            key = "dx" if op == "jvp" else "dq"
+            got[key] = [v + 2.0 * tol * (1.0 + max(abs(x) for x in want[key])) for v in want[key]]
+            assert cp.relaxed_golden_result_gap(got, want) > cp.SUITE_TOL
+    assert cp.kind_tolerance(helpers.load_golden("soc_jvp.json"))[0] == 1e-6
+    assert cp.kind_tolerance(helpers.load_golden("nonneg_jvp.json"))[0] > 1e-3
