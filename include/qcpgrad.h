@@ -118,6 +118,14 @@ int qg_handle_sizes(const qg_handle *h, int64_t *nprob, int64_t *total_n, int64_
  * of SELL-32 slices on the X side (rows of P and A') and on the Y side (rows
  * of A); 0 = that side runs the CSR group-per-row path. */
 int qg_handle_layout(const qg_handle *h, int64_t *sell_slices_x, int64_t *sell_slices_y);
+/* LSMR loop mode chosen at create (diagnostic): *resident = 1 when every
+ * solve runs problem-resident (one persistent kernel, a CTA per problem,
+ * vectors in shared memory: small problems / large batches), 0 = the
+ * 4-launches-per-iteration CUDA-graph loop. */
+int qg_handle_engine(const qg_handle *h, int32_t *resident);
+/* Device time of the LSMR loop (after the init phases) of the last jvp and
+ * the last vjp on this handle, CUDA events on the call's stream (0 = none). */
+int qg_loop_time(const qg_handle *h, double *jvp_ms, double *vjp_ms);
 
 /* jvp: outputs dx (sum n), dy, ds (sum m), diag[nprob] (host). */
 int qg_jvp(qg_handle *h, const qg_perturbation *dtheta, const qg_lsmr_opts *opts,

@@ -69,6 +69,8 @@ _SIGS = {
     "qg_destroy": (ctypes.c_int, [c_vp]),
     "qg_handle_sizes": (ctypes.c_int, [c_vp, P_i64, P_i64, P_i64]),
     "qg_handle_layout": (ctypes.c_int, [c_vp, P_i64, P_i64]),
+    "qg_handle_engine": (ctypes.c_int, [c_vp, ctypes.POINTER(ctypes.c_int32)]),
+    "qg_loop_time": (ctypes.c_int, [c_vp, ctypes.POINTER(c_dbl), ctypes.POINTER(c_dbl)]),
     "qg_jvp": (ctypes.c_int, [c_vp, ctypes.POINTER(PerturbationC), ctypes.POINTER(LsmrOpts),
                               c_vp, c_vp, c_vp, ctypes.POINTER(DiagC), c_vp]),
     "qg_vjp": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, ctypes.POINTER(LsmrOpts),

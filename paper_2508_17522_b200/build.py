@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "_lib")
-SOURCES = ["api.cu", "operator.cu", "assembly.cu", "cones.cu", "transpose.cu", "sell.cu", "comm.cu"]
+SOURCES = ["api.cu", "operator.cu", "assembly.cu", "cones.cu", "transpose.cu", "sell.cu", "comm.cu", "engine.cu"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-fmad=false",

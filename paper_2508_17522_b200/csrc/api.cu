@@ -73,7 +73,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(rk1);
+  dev_free(st); dev_free(d_nactive); dev_free(d_claim); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -99,10 +99,20 @@ static std::map<const Handle *, GraphCache *> g_graphs;
 static std::map<ExecKey, SharedExec> g_exec;
 static std::mutex g_graph_mu;
 
+void Handle::loop_events() {
+  if (!ev_loop[0]) {
+    QG_CUDA(cudaEventCreate(&ev_loop[0]));
+    QG_CUDA(cudaEventCreate(&ev_loop[1]));
+  }
+}
+
 Handle::~Handle() {
+  if (ev_loop[0]) cudaEventDestroy(ev_loop[0]);
+  if (ev_loop[1]) cudaEventDestroy(ev_loop[1]);
   P.release(); Pc.release(); A.release(); AT.release();
   sP.release(); sAT.release(); sA.release();
   dev_free(x_rowof); dev_free(y_rowof);
+  dev_free(c16P); dev_free(c16AT); dev_free(c16A); dev_free(r16x); dev_free(r16y);
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   dev_free(xred); dev_free(psum); dev_free(d_iota);
@@ -226,12 +236,18 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   // cones and Y units
   H.cones.build(d.blocks, d.nblocks, H.yoff, target_rows_y, st);
   trace("cone table");
-  build_sell(H, rpP, rpAT, rpA, st);
+  H.engine = engine_candidate(H);
+  build_sell(H, rpP, rpAT, rpA, H.engine, st);
+  H.engine = H.engine && engine_units_ok(H);
   trace("sell layout");
   H.d_xoff = dev_alloc<int64_t>(B + 1);
   H.d_yoff = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xoff, H.xoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
   QG_CUDA(cudaMemcpyAsync(H.d_yoff, H.yoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+  if (H.engine) {
+    build_engine_layout(H, st);
+    trace("engine layout");
+  }
   H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
   H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xunit_ptr, H.xunit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
@@ -260,6 +276,7 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.part = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
+  W.d_claim = dev_alloc<int>(1);
   W.h_nactive = nullptr;
   if (H.comm) {
     H.xred = dev_alloc<double>(H.NX);
@@ -455,6 +472,11 @@ static void lsmr_finish(Handle &H, qg_diag *diag, cudaStream_t st) {
   std::vector<Lsmr> L(H.B);
   QG_CUDA(cudaMemcpyAsync(L.data(), H.ws.st, sizeof(Lsmr) * H.B, cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
+  if (H.loop_pending) {
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, H.ev_loop[0], H.ev_loop[1]) == cudaSuccess) H.loop_ms[H.loop_pending - 1] = ms;
+    H.loop_pending = 0;
+  }
   for (int p = 0; p < H.B; ++p) {
     if (L[p].status) {
       throw Error{QG_ERR_NUMERICAL, (H.B > 1 ? "problem " + std::to_string(p) + ": " : std::string()) +
@@ -487,8 +509,18 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
   launch_fin(H, M, f0, st);
   UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
   launch_update(H, M, ua, st);
-  run_lsmr_loop(H, M, jvp, cap, st);
-  lsmr_flush(H, M, jvp, st);
+  // the loop is bracketed by events on the call's stream (qg_loop_time; read
+  // back after lsmr_finish's synchronisation)
+  H.loop_events();
+  QG_CUDA(cudaEventRecord(H.ev_loop[0], st));
+  if (H.engine && !H.use_rk1) {
+    launch_engine(H, M, jvp, st);  // the whole loop, problem-resident (engine.cu)
+  } else {
+    run_lsmr_loop(H, M, jvp, cap, st);
+    lsmr_flush(H, M, jvp, st);
+  }
+  QG_CUDA(cudaEventRecord(H.ev_loop[1], st));
+  H.loop_pending = jvp ? 1 : 2;
 }
 
 }  // namespace qg
@@ -558,6 +590,20 @@ int qg_handle_layout(const qg_handle *h, int64_t *sell_slices_x, int64_t *sell_s
   const Handle *H = reinterpret_cast<const Handle *>(h);
   *sell_slices_x = H->nslice_x;
   *sell_slices_y = H->nslice_y;
+  QG_API_END
+}
+
+int qg_handle_engine(const qg_handle *h, int32_t *resident) {
+  QG_API_BEGIN_NS
+  *resident = reinterpret_cast<const Handle *>(h)->engine ? 1 : 0;
+  QG_API_END
+}
+
+int qg_loop_time(const qg_handle *h, double *jvp_ms, double *vjp_ms) {
+  QG_API_BEGIN_NS
+  const Handle *H = reinterpret_cast<const Handle *>(h);
+  *jvp_ms = H->loop_ms[0];
+  *vjp_ms = H->loop_ms[1];
   QG_API_END
 }
 

@@ -311,7 +311,10 @@ void ConeTable::build(const qg_cone_block *blocks, const int64_t *nblocks, const
             if (cls == CLS_SOC) {  // thread-per-block fused epilogue for small SOC blocks
               int maxdim = 0;
               for (int64_t k = bi; k < e; ++k) maxdim = std::max(maxdim, (int)h_blk[k].dim);
-              un.group = maxdim <= 32 ? 1 : 0;
+              // lanes per block of the engine's group epilogue (power of two >= dim)
+              int g = 1;
+              while (g < maxdim) g <<= 1;
+              un.group = maxdim <= 32 ? g : 0;
             }
             out.push_back(un);
             bi = e;

@@ -47,6 +47,20 @@ __device__ __forceinline__ void soc_apply_warp(const double *zb, int dim, double
   }
 }
 
+// Entry i of the SOC derivative applied to dt (cones.py:740-764) for a block
+// with t0 = z[0], nu = ||z[1:]||, udu = z[1:]'dt[1:], di = dt[i], zi = z[i];
+// code: 0 zero map, 1 identity, 2 half, 3 formula.
+__device__ __forceinline__ double soc_entry(int code, int i, double nu, double t0, double zi, double di,
+                                            double dt, double udu) {
+  if (code == 0) return 0.0;
+  if (code == 1) return di;
+  if (code == 2) return 0.5 * di;
+  const double two_nu = 2.0 * nu;
+  if (i == 0) return (nu * dt + udu) / two_nu;
+  const double c = (t0 / (nu * nu)) * udu;
+  return ((zi * dt + (t0 + nu) * di) - c * zi) / two_nu;
+}
+
 // d x d product C = sum_k a(i,k) b(k,j) with TI x TJ register tiles per
 // thread (TI + TJ shared-memory loads per TI*TJ FMAs); out(i, j, c) stores.
 // lower = true: only tiles touching the lower triangle (j <= i) are computed

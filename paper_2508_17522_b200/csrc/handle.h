@@ -62,6 +62,7 @@ struct Workspace {
   double *rk1 = nullptr;     // EVec: refine rank-one vector (allocated on first use)
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
+  int *d_claim = nullptr;    // problem claim counter of the resident engine
   int *h_nactive = nullptr;  // pinned
   void release();
 };
@@ -80,6 +81,10 @@ struct Handle {
   int32_t *y_rowof = nullptr;
   int64_t nslice_x = 0, nslice_y = 0;
   bool has_wide = false;        // some unit runs CTA-per-row (MODE_WIDE)
+  bool engine = false;          // LSMR solves run problem-resident (engine.cu)
+  // engine layout: 16-bit problem-local columns parallel to the SELL entries
+  // of P, A', A and 16-bit local rows of the slice lanes (0xffff = padding)
+  uint16_t *c16P = nullptr, *c16AT = nullptr, *c16A = nullptr, *r16x = nullptr, *r16y = nullptr;
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;
@@ -103,6 +108,12 @@ struct Handle {
   bool deriv_ready = true;  // D Pi prepared at the current point
   bool use_rk1 = false;     // LSMR on J = F - rk1 e_N' (qg_lsmr_jacobian)
 
+  // device time of the last jvp / vjp LSMR loop (qg_loop_time)
+  cudaEvent_t ev_loop[2] = {nullptr, nullptr};
+  double loop_ms[2] = {0.0, 0.0};
+  int loop_pending = 0;  // 1: jvp, 2: vjp events recorded, not yet read
+  void loop_events();
+
   int nxu() const { return (int)xunits.size(); }
   int nyu() const { return (int)cones.units.size(); }
   ~Handle();
@@ -120,6 +131,14 @@ void csc_to_csr(const CscBatch &in, DevCsr &out, DevCsr *csc_as_rows, bool keep_
 
 // SELL copies of P, A' (X units) and A (Y units); sets unit modes / slices
 // (sell.cu).  rp* are host copies of the CSR row pointers.
-void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, cudaStream_t st);
+// force: SELL on both sides (the resident engine walks SELL slices only).
+void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, bool force, cudaStream_t st);
+
+// Problem-resident LSMR engine (engine.cu): whether a batch qualifies
+// (before the SELL build), whether every unit ended up SELL (after), and the
+// launch that runs the whole loop of a solve after its init phases.
+bool engine_candidate(const Handle &H);
+bool engine_units_ok(const Handle &H);
+void build_engine_layout(Handle &H, cudaStream_t st);
 
 }  // namespace qg

@@ -12,6 +12,7 @@
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
 #include "dpi_dev.cuh"
+#include "lsmr_dev.cuh"
 #include "ops_dev.cuh"
 #include "operator.h"
 
@@ -175,20 +176,8 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
 }
 
 // F'-step epilogue for a unit of SOC blocks of dim <= 32: one thread per
-// block (cones.py:740-764 applied twice): udu = u'dt ; r = D Pi t ; o = row
-// update ; udu2 = u'o ; D Pi o.  Entries stream through L1 in three short
-// passes with independent loads (no shuffles, no CTA barrier).
-__device__ __forceinline__ double soc_entry(int code, int i, double nu, double t0, double zi, double di,
-                                            double dt, double udu) {
-  if (code == 0) return 0.0;
-  if (code == 1) return di;
-  if (code == 2) return 0.5 * di;
-  const double two_nu = 2.0 * nu;
-  if (i == 0) return (nu * dt + udu) / two_nu;
-  const double c = (t0 / (nu * nu)) * udu;
-  return ((zi * dt + (t0 + nu) * di) - c * zi) / two_nu;
-}
-
+// block (soc_entry, dpi_dev.cuh, applied twice).  Entries stream through L1
+// in three short passes with independent loads (no shuffles, no CTA barrier).
 template <class Fin>
 __device__ __forceinline__ void soc_epilogue(const DpiView &dv, const Unit &u, const double *t, Fin fin_row,
                                              const double *outY, double *dpout) {
@@ -425,62 +414,6 @@ __global__ void __launch_bounds__(kThreads) k_update(Mats M, UpdArgs a) {
     for (int k = 0; k < kSlots; ++k) a.part[(size_t)blockIdx.x * kSlots + k] = tot[k];
 }
 
-// ----------------------------------------------------------- finalize --
-__device__ __forceinline__ double dsign(double v) { return (v > 0.0) ? 1.0 : ((v < 0.0) ? -1.0 : 0.0); }
-
-__device__ __forceinline__ void sym_ortho(double a, double b, double &c, double &s, double &r) {   // lsmr.py:38-54
-  if (b == 0.0) { c = dsign(a); s = 0.0; r = fabs(a); return; }
-  if (a == 0.0) { c = 0.0; s = dsign(b); r = fabs(b); return; }
-  if (fabs(b) > fabs(a)) {
-    const double t = a / b;
-    s = dsign(b) / sqrt(1.0 + t * t);
-    c = s * t;
-    r = b / s;
-  } else {
-    const double t = b / a;
-    c = dsign(a) / sqrt(1.0 + t * t);
-    s = c * t;
-    r = a / c;
-  }
-}
-
-// T component of an operator step output (embedding.py:232-237, 261 and 420-425).
-__device__ __forceinline__ double t_component(int kind, const Embed &E, double wN, const double sx[kSlots],
-                                              const double sy[kSlots]) {
-  if (kind == STEP_F) {
-    const double outN = ((-(2.0 / E.tau)) * sx[0] - sx[1] - sy[0]) + (E.xPx / (E.tau * E.tau)) * wN;
-    return ((outN - E.last * wN) + wN) / E.zN;
-  }
-  const double gN = (sx[1] + sy[0]) + (E.xPx / (E.tau * E.tau)) * wN;
-  return (E.last * (gN - wN) + wN) / E.zN;
-}
-
-// Stopping rules after iteration itn with ||x||^2 = xx + xN^2 (lsmr.py:168-184).
-// Returns true when the solve ended (problem deactivated).
-__device__ __forceinline__ bool stop_test(Lsmr *L, double xx, double xN) {
-  const double normx = sqrt(xx + xN * xN);
-  L->normx = normx;
-  const double normr = L->normr, normar = L->normar, normA = L->normA, normb = L->normb;
-  if (!(isfinite(normr) && isfinite(normar) && isfinite(normx))) {
-    L->status = QG_ERR_NUMERICAL;
-    L->active = 0;
-    return true;
-  }
-  bool stop = false;
-  if (normar == 0.0) stop = true;
-  else {
-    const double test1 = normr / normb;
-    const double test2 = normr > 0.0 ? normar / (normA * normr) : 0.0;
-    const double rtol = L->btol + L->atol * normA * normx / normb;
-    const double t1 = test1 / (1.0 + normA * normx / normb);
-    if (1.0 + test2 <= 1.0 || 1.0 + t1 <= 1.0) stop = true;
-    else if (test2 <= L->atol || test1 <= rtol) stop = true;
-  }
-  if (stop) { L->active = 0; L->converged = 1; return true; }
-  if (L->itn >= L->max_iter) { L->active = 0; L->converged = 0; return true; }
-  return false;
-}
-
 // Per-problem sums of the unit partials in exactly k_fin's order (row-
 // partitioned mode): psum = [X sums: B x kSlots | Y sums: B x kSlots].
 __global__ void k_part_reduce(const double *px, const int64_t *px_ptr, const double *py, const int64_t *py_ptr,
@@ -516,6 +449,8 @@ __device__ __forceinline__ bool fin_skips(const FinArgs &a, int p) {
 // finalize); else the warp reduces them (all 32 lanes call).  Lsh: a
 // shared-memory copy of the problem's LSMR state to work on (the caller
 // loads and stores it cooperatively), else the state in global memory.
+// The scalar work is fin_core (lsmr_dev.cuh) on the T entries of the
+// vectors, loaded here and stored back where fin_core wrote them.
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
                                             const double *pre = nullptr, Lsmr *Lsh = nullptr) {
   Lsmr *L = Lsh ? Lsh : (a.st ? a.st + p : nullptr);
@@ -538,175 +473,20 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
     for (int j = 0; j < kSlots; ++j) { sx[j] = warp_sum(sx[j]); sy[j] = warp_sum(sy[j]); }
   }
   if (lane != 0) return;
-  const Embed E = M.emb[p];
   const int64_t T = M.NX + M.NY + p;
-  // T component of the step output, with the refine rank-one term
-  // (testkit.py:446-451): F: - r_N w_N ; F': - r'w
-  auto tcomp = [&](double wN) {
-    double t = t_component(a.kind, E, wN, sx, sy);
-    if (a.rk1) t -= (a.kind == STEP_F) ? a.rk1[T] * wN : (sx[3] + sy[3]) + a.rk1[T] * wN;
-    return t;
-  };
-
-  if (a.phase == PH_APPLY) {
-    a.out[T] = tcomp(a.in[T]);
-    return;
-  }
-  if (a.phase == PH_RHS) {
-    // rhs_N from the assembly partials; then lsmr.py:72-80
-    double rN;
-    if (a.kind == RHS_JVP) {
-      const double outN = ((-sx[0]) / E.tau - sx[1]) - sy[0];   // embedding.py:291
-      rN = (-outN) / fabs(E.zN);
-    } else if (a.kind == RHS_VEC) {
-      rN = a.in[T];                                             // given right-hand side
-    } else {
-      const double dzN = ((-sx[0]) - sy[0]) - sy[1];             // solution_map.py:259
-      rN = -dzN;
-    }
-    a.out[T] = rN;
-    const double beta = sqrt((sx[2] + sy[2]) + rN * rN);
-    L->beta = beta;
-    L->normb = beta;
-    L->itn = 0;
-    L->status = 0;
-    L->skip_v = 0;
-    L->alpha = 0.0;
-    L->s_v = 1.0;
-    if (beta > 0.0) {
-      L->s_u = 1.0 / beta;
-      L->s_in = L->s_u;
-      L->c_out = 0.0;
-      L->active = 1;
-    } else {
-      L->s_u = 1.0;
-      L->active = 0;
-      L->converged = 1;
-      L->normr = beta;
-      L->normar = 0.0;
-    }
-    return;
-  }
-  if (a.phase == PH_INIT_V) {
-    const double vN = tcomp(a.in[T]) * L->s_in;
-    a.out[T] = vN;
-    const double alpha = sqrt((sx[2] + sy[2]) + vN * vN);
-    L->alpha = alpha;
-    L->s_v = alpha > 0.0 ? 1.0 / alpha : 1.0;
-    const double beta = L->beta;
-    if (alpha * beta == 0.0) {
-      L->active = 0;
-      L->converged = 1;
-      L->normr = beta;
-      L->normar = 0.0;
-      return;
-    }
-    L->zetabar = alpha * beta;
-    L->alphabar = alpha;
-    L->rho = L->rhobar = L->cbar = 1.0;
-    L->sbar = 0.0;
-    L->betadd = beta;
-    L->betad = 0.0;
-    L->rhodold = 1.0;
-    L->tautildeold = L->thetatilde = L->zeta = L->d = 0.0;
-    L->normA2 = alpha * alpha;
-    L->normr = beta;
-    L->normar = alpha * beta;
-    L->c_hbar = L->c_x = L->c_h = 0.0;
-    a.h[T] = vN * L->s_v;
-    a.hb[T] = 0.0;
-    a.x[T] = 0.0;
-    L->s_in = L->s_v;
-    L->c_out = alpha * L->s_u;
-    if (L->max_iter <= 0) { L->active = 0; L->converged = 0; }
-    return;
-  }
-  if (a.phase == PH_STEP_U) {
-    if (L->itn > 0 && stop_test(L, sx[3] + sy[3], a.x[T])) return;  // iteration itn ended the solve
-    L->itn += 1;
-    const double uN = L->s_in * tcomp(a.in[T]) - L->c_out * a.old[T];
-    a.out[T] = uN;
-    const double beta = sqrt((sx[2] + sy[2]) + uN * uN);
-    L->beta = beta;
-    if (beta > 0.0) {
-      L->s_u = 1.0 / beta;
-      L->skip_v = 0;
-      L->s_in = L->s_u;
-      L->c_out = beta * L->s_v;
-    } else {
-      L->s_u = 1.0;
-      L->skip_v = 1;
-    }
-    return;
-  }
-  if (a.phase == PH_STEP_V) {
-    double alpha = L->alpha;
-    if (!L->skip_v) {
-      const double vN = L->s_in * tcomp(a.in[T]) - L->c_out * a.old[T];
-      a.out[T] = vN;
-      alpha = sqrt((sx[2] + sy[2]) + vN * vN);
-      L->alpha = alpha;
-      L->s_v = alpha > 0.0 ? 1.0 / alpha : 1.0;
-    }
-    const double beta = L->beta;
-    if (!(isfinite(alpha) && isfinite(beta))) {
-      L->status = QG_ERR_NUMERICAL;
-      L->active = 0;
-      return;
-    }
-    // lsmr.py:127-171
-    double chat, shat, alphahat;
-    sym_ortho(L->alphabar, 0.0, chat, shat, alphahat);
-    const double rhoold = L->rho;
-    double c, s, rho;
-    sym_ortho(alphahat, beta, c, s, rho);
-    const double thetanew = s * alpha;
-    L->alphabar = c * alpha;
-    const double rhobarold = L->rhobar;
-    const double zetaold = L->zeta;
-    const double thetabar = L->sbar * rho;
-    const double rhotemp = L->cbar * rho;
-    double cbar, sbar, rhobar;
-    sym_ortho(rhotemp, thetanew, cbar, sbar, rhobar);
-    const double zeta = cbar * L->zetabar;
-    L->zetabar = -sbar * L->zetabar;
-    L->c_hbar = thetabar * rho / (rhoold * rhobarold);
-    L->c_x = zeta / (rho * rhobar);
-    L->c_h = thetanew / rho;
-    const double betaacute = chat * L->betadd;
-    const double betacheck = -shat * L->betadd;
-    const double betahat = c * betaacute;
-    L->betadd = -s * betaacute;
-    const double thetatildeold = L->thetatilde;
-    double ctildeold, stildeold, rhotildeold;
-    sym_ortho(L->rhodold, thetabar, ctildeold, stildeold, rhotildeold);
-    L->thetatilde = stildeold * rhobar;
-    L->rhodold = ctildeold * rhobar;
-    L->betad = -stildeold * L->betad + ctildeold * betahat;
-    L->tautildeold = (zetaold - thetatildeold * L->tautildeold) / rhotildeold;
-    const double taud = (zeta - L->thetatilde * L->tautildeold) / L->rhodold;
-    L->d = L->d + betacheck * betacheck;
-    const double bt = L->betad - taud;
-    L->normr = sqrt(L->d + bt * bt + L->betadd * L->betadd);
-    L->normA2 = L->normA2 + beta * beta;
-    L->normA = sqrt(L->normA2);
-    L->normA2 = L->normA2 + alpha * alpha;
-    L->normar = fabs(L->zetabar);
-    L->rho = rho;
-    L->rhobar = rhobar;
-    L->cbar = cbar;
-    L->sbar = sbar;
-    L->zeta = zeta;
-    // T parts of the vector updates
-    const double hb = a.h[T] - L->c_hbar * a.hb[T];
-    a.x[T] = a.x[T] + L->c_x * hb;
-    a.h[T] = a.v[T] * L->s_v - L->c_h * a.h[T];
-    a.hb[T] = hb;
-    L->s_in = L->s_v;
-    L->c_out = alpha * L->s_u;
-    return;
-  }
-  if (a.phase == PH_STEP_X) stop_test(L, sx[0] + sy[0], a.x[T]);
+  TVals t;
+  t.in = a.in ? a.in[T] : 0.0;
+  t.old = a.old ? a.old[T] : 0.0;
+  t.out = t.old;
+  t.h = (a.phase == PH_STEP_V) ? a.h[T] : 0.0;
+  t.hb = (a.phase == PH_STEP_V) ? a.hb[T] : 0.0;
+  t.x = (a.phase == PH_STEP_V || a.phase == PH_STEP_U || a.phase == PH_STEP_X) ? a.x[T] : 0.0;
+  t.rk1 = a.rk1 ? a.rk1[T] : 0.0;
+  const int w = fin_core(M.emb[p], a.phase, a.kind, L, sx, sy, t, a.rk1 != nullptr, true);
+  if (w & TV_OUT) a.out[T] = t.out;
+  if (w & TV_H) a.h[T] = t.h;
+  if (w & TV_HB) a.hb[T] = t.hb;
+  if (w & TV_X) a.x[T] = t.x;
 }
 
 __global__ void k_fin(Mats M, FinArgs a) {

@@ -235,7 +235,8 @@ int64_t build_side(std::vector<Unit> &units, Unit *d_units, int64_t nrows, const
 
 }  // namespace
 
-void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, cudaStream_t st) {
+void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_t *rpA, bool force_sell,
+                cudaStream_t st) {
   // Thread-per-row SELL pays off when a side has many short rows: enough
   // slices to fill the GPU with warps and rows short enough that a thread's
   // serial chain stays short.  Otherwise the side keeps G-lanes-per-row CSR
@@ -243,6 +244,7 @@ void build_sell(Handle &H, const int32_t *rpP, const int32_t *rpAT, const int32_
   const char *force = std::getenv("QG_SELL");
   auto sell_ok = [&](int64_t rows, int64_t nnz) {
     if (force) return std::atoi(force) != 0;
+    if (force_sell) return true;
     const double avg = rows ? (double)nnz / rows : 0.0;
     return rows / 32 >= kMinSellSlices && avg <= 64.0;
   };

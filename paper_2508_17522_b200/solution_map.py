@@ -214,6 +214,20 @@ class QCPBatch:
         N.check(N.lib().qg_handle_layout(self._h, N.ctypes.byref(sx), N.ctypes.byref(sy)))
         return int(sx.value), int(sy.value)
 
+    def resident(self):
+        """True when this batch's LSMR solves run problem-resident (one
+        persistent kernel, a CTA per problem, vectors in shared memory)."""
+        r = N.ctypes.c_int32()
+        N.check(N.lib().qg_handle_engine(self._h, N.ctypes.byref(r)))
+        return bool(r.value)
+
+    def loop_time(self):
+        """(jvp ms, vjp ms): device time of the last LSMR loops on this batch
+        (CUDA events on the call's stream, after the init phases)."""
+        j, v = N.ctypes.c_double(), N.ctypes.c_double()
+        N.check(N.lib().qg_loop_time(self._h, N.ctypes.byref(j), N.ctypes.byref(v)))
+        return float(j.value), float(v.value)
+
     def time_kernel(self, which, reps=20):
         """Mean device ms per launch of a hot kernel (0: F step, 1: F' step,
         2: LSMR update), CUDA events on the current stream."""

@@ -11,6 +11,7 @@ import sys
 rep = sys.argv[1]
 kern = sys.argv[2] if len(sys.argv) > 2 else ""
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+col = sys.argv[4] if len(sys.argv) > 4 else "Warp Stall Sampling (All Samples)"  # or "Instructions Executed"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--print-source", "cuda,sass", "--csv"],
                      capture_output=True, text=True).stdout
 agg = collections.Counter()
@@ -28,7 +29,7 @@ for row in csv.reader(io.StringIO(out)):
         fn = row[1]
         continue
     if row[0] == "Line No":
-        si = row.index("Warp Stall Sampling (All Samples)")
+        si = row.index(col)
         continue
     if kern and (fn is None or kern not in fn):
         continue
