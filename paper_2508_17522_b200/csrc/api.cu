@@ -112,7 +112,7 @@ Handle::~Handle() {
   P.release(); Pc.release(); A.release(); AT.release();
   sP.release(); sAT.release(); sA.release();
   dev_free(x_rowof); dev_free(y_rowof);
-  dev_free(c16P); dev_free(c16AT); dev_free(c16A); dev_free(r16x); dev_free(r16y);
+  dev_free(c16P); dev_free(c16AT); dev_free(c16A); dev_free(eng_blob); dev_free(eng_prof);
   dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   dev_free(xred); dev_free(psum); dev_free(d_iota);
@@ -244,14 +244,14 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   H.d_yoff = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xoff, H.xoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
   QG_CUDA(cudaMemcpyAsync(H.d_yoff, H.yoff.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
-  if (H.engine) {
-    build_engine_layout(H, st);
-    trace("engine layout");
-  }
   H.d_xunit_ptr = dev_alloc<int64_t>(B + 1);
   H.d_yunit_ptr = dev_alloc<int64_t>(B + 1);
   QG_CUDA(cudaMemcpyAsync(H.d_xunit_ptr, H.xunit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
   QG_CUDA(cudaMemcpyAsync(H.d_yunit_ptr, H.cones.unit_ptr.data(), sizeof(int64_t) * (B + 1), cudaMemcpyHostToDevice, st));
+  if (H.engine) {
+    build_engine_layout(H, st);
+    trace("engine layout");
+  }
 
   // problem vectors
   H.q = dev_alloc<double>(H.NX);

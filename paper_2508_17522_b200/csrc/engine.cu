@@ -1,40 +1,42 @@
 // Problem-resident LSMR engine: batches of small problems (c5a: 4096 QCPs
 // of n=1000, m=1500; c1) run their WHOLE solve inside one persistent kernel.
 //
-// One 1024-thread CTA per SM owns one problem at a time (claimed from a
-// counter) and runs every remaining LSMR iteration of it (lsmr.py:111-184)
-// without leaving the SM.  Shared memory holds
+// One CTA (512 threads, one per SM; QG_ENG_CFG) owns one problem at
+// a time (claimed from a counter) and runs every remaining LSMR iteration of
+// it (lsmr.py:111-184) without leaving the SM.  Shared memory holds
 //
-//   u[N] | v[N] | rs[n+m] | dp[m]        the LSMR vectors (N = n+m+1, T entry
-//                                        at n+m), row sums, D Pi of the F input
-//   resident matrix part                 a slice prefix of each of the
-//                                        problem's SELL-32 matrices P, A, A'
-//                                        (fp64 values + 16-bit local column
-//                                        indices), loaded ONCE per problem by
-//                                        TMA bulk copies (cp.async.bulk +
-//                                        mbarrier complete_tx)
+//   u[N] | v[N] | rs[N] | dp[m]   the LSMR vectors (N = n+m+1, T entry at
+//                                 n+m), row sums, D Pi of the F input
+//   meta blob                     the problem's slice table (widths, offsets,
+//                                 16-bit rows), Y work units and cone blocks
+//                                 (built once at preparation, k_engine_meta)
+//   resident matrix part          a slice prefix of each of the problem's
+//                                 SELL-32 matrices P, A, A' (fp64 values +
+//                                 16-bit local columns)
 //
-// and the rest of the matrix streams from HBM / L2 every operator
-// application with read-only no-L1-allocate loads.  With one problem per SM
-// the streamed parts of all resident problems (~150 x 160 KB at c5a) stay in
-// L2 across the solve's 200 applications.
+// the blob and the resident part arrive by TMA bulk copies (cp.async.bulk +
+// one mbarrier complete_tx phase per problem); the rest of the matrix
+// streams from L2 every operator application with an L2 evict-last policy
+// (~150 problems x 160 KB stay L2-resident across their 200 applications).
 //
 // Iteration (the graph path's order: the vector update of iteration k runs
 // fused into the u-step epilogue of k+1, its stop test before fin U):
 //
-//   A_u  SpMV of v (all slices, dynamic claims)  ||  warp 0: sums + fin V(k-1)
+//   A_u  SpMV of v (static slice pairs per warp)  ||  warp 0: sums + fin V(k-1)
 //   B_u  u-step row epilogue + update of h, hbar, x (lsmr.py:142-144)
-//   A_v  SpMV of u                               ||  warp 0: sums + stop test + fin U
+//   A_v  SpMV of u                                ||  warp 0: sums + stop test + fin U
 //   B_v  v-step row epilogue (+ D Pi of the F' step per cone block)
 //
 // so the scalar finalize (thread 0: norms, Givens recurrences, stopping
-// rules) overlaps the next SpMV phase instead of idling the SM; 4 CTA
-// barriers per iteration, no kernel launch, no grid-wide barrier, no host
-// round trip; a finished problem frees its CTA for the next claim at once.
+// rules) overlaps the next SpMV phase; 4 CTA barriers per iteration, no
+// kernel launch, no grid-wide barrier, no host round trip; a finished
+// problem frees its CTA for the next claim at once.
 //
 // The arithmetic of every row / block / scalar is the graph path's
 // (operator.cu expressions, fin_core through lsmr_dev.cuh); only the CTA
 // summation trees differ (deterministic, fixed order).
+#include <cstdio>
+
 #include "dpi_dev.cuh"
 #include "lsmr_dev.cuh"
 #include "ops_dev.cuh"
@@ -42,31 +44,61 @@
 
 namespace qg {
 
-constexpr int kEngMaxWarps = 32;  // CTAs of 1024 threads (one per SM) or 512 (two per SM, QG_ENG_THREADS=512)
+constexpr int kEngMaxWarps = 32;
 constexpr uint16_t kPad16 = 0xffff;
 #ifndef QG_ENG_UNROLL
-#define QG_ENG_UNROLL 8
+#define QG_ENG_UNROLL 4
 #endif
+
+// ---------------------------------------------------------- meta blob --
+// Per problem, fixed stride (the batch maximum), 16-byte aligned sections.
+struct EngHead {
+  int32_t nxs, nys, nyu, nblk;     // X / Y slices, Y units, cone blocks
+  int32_t res[3];                  // resident slice count of P, A', A
+  int32_t soff[3];                 // their smem entry offsets
+  int32_t ent[3];                  // their resident entries
+  int32_t pad;
+  int64_t g0[3];                   // first entry of each matrix region
+};
+struct SliceMeta {                 // X slice: P part (off0, w0), A' part (off1, w1); Y slice: A part in (off1, w1)
+  int32_t off0, off1;              // entry offsets from the region start
+  uint16_t w0, w1;
+};
+struct EUnit {                     // a Y work unit, local rows / blocks
+  int32_t cls, kind, G, row0, row1, blk0, blk1, pad;
+};
+struct EBlk {                      // a cone block: parameter index, local row, dim
+  int32_t param;
+  uint16_t j0, dim;
+};
+struct BlobLayout {
+  int smax, umax, bmax;
+  size_t o_slices, o_rows, o_units, o_blks, stride;
+};
+static __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
+static __host__ __device__ inline BlobLayout blob_layout(int smax, int umax, int bmax) {
+  BlobLayout L{smax, umax, bmax, 0, 0, 0, 0, 0};
+  L.o_slices = al16(sizeof(EngHead));
+  L.o_rows = al16(L.o_slices + sizeof(SliceMeta) * (size_t)smax);
+  L.o_units = al16(L.o_rows + sizeof(uint16_t) * 32 * (size_t)smax);
+  L.o_blks = al16(L.o_units + sizeof(EUnit) * (size_t)umax);
+  L.stride = al16(L.o_blks + sizeof(EBlk) * (size_t)bmax);
+  return L;
+}
 
 struct EngArgs {
   Lsmr *st;
   double *u, *v, *h, *hb, *x;  // EVec workspace (global)
   const double *dp0;           // Y layout: D Pi of the first F step's input (jvp: dpv; vjp: unused)
   const uint16_t *c16P, *c16AT, *c16A;  // 16-bit local columns parallel to the SELL entries
-  const uint16_t *r16x, *r16y;          // 16-bit local row of every slice lane (kPad16 = padding)
+  const unsigned char *blob;   // per-problem meta blobs
+  BlobLayout bl;
   int *next;                   // problem claim counter (zeroed before the launch)
   int B;
   int nmax, mmax;              // vector strides (max n+m+1, max m over the batch)
-  int vec_doubles;             // 3 nmax + mmax rounded up to even (16-byte aligned resident area)
-  int res_cap;                 // resident matrix capacity in entries (multiple of 8)
-};
-
-// One SELL matrix of the resident problem: slices [s0, s1); the prefix
-// [s0, sres) sits in shared memory at entry offset soff.
-struct Region {
-  int64_t g0;        // first entry (S.off[s0])
-  int s0, s1, sres;
-  int soff;
+  int vec_doubles;             // 3 nmax + mmax rounded up to even
+  int res_cap;                 // resident matrix capacity in entries (multiple of 32)
+  unsigned long long *prof;    // QG_ENG_PROF=1: SM cycles [setup, A_u, B_u, A_v, B_v, iters, fin, spmv(warp 1)]
 };
 
 struct EngShared {
@@ -74,8 +106,8 @@ struct EngShared {
   double red[kEngMaxWarps * 2 * kSlots];
   double tvh[3];      // T entries of h, hbar, x
   unsigned long long mbar;
-  Region reg[3];      // P, A' (X slices), A (Y slices)
-  int p, cnt[2], rescount;
+  unsigned long long prof[8];
+  int p;
 };
 
 // ------------------------------------------------------------ TMA bulk --
@@ -119,72 +151,179 @@ __device__ __forceinline__ uint16_t ld_keep16(const uint16_t *p, uint64_t pol) {
   return v;
 }
 
-// Row sum of this lane's row in slice s of region R: resident slices read
-// values / columns from shared memory, the others stream them from global
-// memory; the gather reads the shared-memory vector `vec` (local columns).
-template <int UNR>
-__device__ __forceinline__ double slice_dot(const Region &R, const SellView &S, const uint16_t *c16, int s, int lane,
-                                            const double *vec, const double *sv, const uint16_t *sc) {
-  const int w = S.w[s];
-  const int64_t off = S.off[s];
-  double a = 0.0;
-  if (s < R.sres) {
-    const int base = R.soff + (int)(off - R.g0) + lane;
-    const double *vp = sv + base;
-    const uint16_t *cp = sc + base;
-#pragma unroll 4
-    for (int k = 0; k < w; ++k) a += vp[32 * k] * vec[cp[32 * k]];
-  } else {
-    // every load of an UNR-entry group in flight at once (predicated tail:
-    // no serial remainder chain); sums stay in storage order
-    const double *vp = S.val + off + lane;
-    const uint16_t *cp = c16 + off + lane;
-    const uint64_t pol = l2_keep_policy();
-    for (int k = 0; k < w; k += UNR) {
-      double vv[UNR];
-      uint16_t cc[UNR];
+// Per-problem views of the shared-memory blob and resident area, derived
+// on demand from the kernel parameters (constant bank) so they hold no
+// registers across the loop.
+struct EngView {
+  const Mats &M;
+  const EngArgs &a;
+  __device__ __forceinline__ unsigned char *blob() const {
+    extern __shared__ __align__(16) double sm[];
+    return reinterpret_cast<unsigned char *>(sm + a.vec_doubles);
+  }
+  __device__ __forceinline__ const EngHead *hd() const { return reinterpret_cast<const EngHead *>(blob()); }
+  __device__ __forceinline__ const SliceMeta *sl() const {
+    return reinterpret_cast<const SliceMeta *>(blob() + a.bl.o_slices);
+  }
+  __device__ __forceinline__ const uint16_t *rows() const {
+    return reinterpret_cast<const uint16_t *>(blob() + a.bl.o_rows);
+  }
+  __device__ __forceinline__ const EUnit *units() const { return reinterpret_cast<const EUnit *>(blob() + a.bl.o_units); }
+  __device__ __forceinline__ const EBlk *blks() const { return reinterpret_cast<const EBlk *>(blob() + a.bl.o_blks); }
+  __device__ __forceinline__ double *resv() const { return reinterpret_cast<double *>(blob() + a.bl.stride); }
+  __device__ __forceinline__ uint16_t *resc() const { return reinterpret_cast<uint16_t *>(resv() + a.res_cap); }
+  __device__ __forceinline__ const double *gval(int r) const {
+    return (r == 0 ? M.sP.val : r == 1 ? M.sAT.val : M.sA.val) + hd()->g0[r];
+  }
+  __device__ __forceinline__ const uint16_t *gcol(int r) const {
+    return (r == 0 ? a.c16P : r == 1 ? a.c16AT : a.c16A) + hd()->g0[r];
+  }
+};
+
+// Loads of one entry of a slice lane: shared memory (resident) or global
+// with the L2 evict-last policy (streamed).
+template <bool RES>
+__device__ __forceinline__ double ldv(const double *p, uint64_t pol) {
+  if constexpr (RES) return *p;
+  else return ld_keep(p, pol);
+}
+template <bool RES>
+__device__ __forceinline__ uint16_t ldc(const uint16_t *p, uint64_t pol) {
+  if constexpr (RES) return *p;
+  else return ld_keep16(p, pol);
+}
+
+// Row sums of this lane's rows in two slices (widths wa, wb; wb = 0: no
+// second slice).  SELL padding (value 0, local column 0) makes every lane
+// valid up to its slice width, so the loops carry no per-entry predicate:
+// 4-entry groups of both slices issue all their loads before any gather.
+// Each sum runs in storage order.
+template <bool RA, bool RB>
+__device__ __forceinline__ void dot2(const double *va, const uint16_t *ca, int wa, const double *vb,
+                                     const uint16_t *cb, int wb, const double *vec, double &sa, double &sb) {
+  const uint64_t pol = (RA && RB) ? 0 : l2_keep_policy();
+  double a = 0.0, b = 0.0;
+  const int wm = wa < wb ? wa : wb;
+  int k = 0;
+  for (; k + 4 <= wm; k += 4) {
+    double xa[4], xb[4];
+    uint16_t ka[4], kb[4];
 #pragma unroll
-      for (int j = 0; j < UNR; ++j) {
-        const bool ok = k + j < w;
-        vv[j] = ok ? ld_keep(vp + 32 * (k + j), pol) : 0.0;
-        cc[j] = ok ? ld_keep16(cp + 32 * (k + j), pol) : (uint16_t)0;
-      }
+    for (int j = 0; j < 4; ++j) {
+      xa[j] = ldv<RA>(va + 32 * (k + j), pol);
+      ka[j] = ldc<RA>(ca + 32 * (k + j), pol);
+      xb[j] = ldv<RB>(vb + 32 * (k + j), pol);
+      kb[j] = ldc<RB>(cb + 32 * (k + j), pol);
+    }
 #pragma unroll
-      for (int j = 0; j < UNR; ++j)
-        if (k + j < w) a += vv[j] * vec[cc[j]];
+    for (int j = 0; j < 4; ++j) {
+      a += xa[j] * vec[ka[j]];
+      b += xb[j] * vec[kb[j]];
     }
   }
-  return a;
+  for (; k < wm; ++k) {
+    const double x1 = ldv<RA>(va + 32 * k, pol), x2 = ldv<RB>(vb + 32 * k, pol);
+    const uint16_t k1 = ldc<RA>(ca + 32 * k, pol), k2 = ldc<RB>(cb + 32 * k, pol);
+    a += x1 * vec[k1];
+    b += x2 * vec[k2];
+  }
+  int j = wm;
+  for (; j + 4 <= wa; j += 4) {
+    double xa[4];
+    uint16_t ka[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      xa[i] = ldv<RA>(va + 32 * (j + i), pol);
+      ka[i] = ldc<RA>(ca + 32 * (j + i), pol);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a += xa[i] * vec[ka[i]];
+  }
+  for (; j < wa; ++j) a += ldv<RA>(va + 32 * j, pol) * vec[ldc<RA>(ca + 32 * j, pol)];
+  for (int i = wm; i < wb; ++i) b += ldv<RB>(vb + 32 * i, pol) * vec[ldc<RB>(cb + 32 * i, pol)];
+  sa = a;
+  sb = b;
+}
+
+// Two slices of region r (0: P, 1: A', 2: A) at entry offsets oa / ob and
+// widths wa / wb (wb = 0: none); slice a resident iff ra (b resident only if
+// a is: resident slices are a prefix and qa < qb).
+__device__ __forceinline__ void region_dot2(const EngView &V, int r, bool ra, int oa, int wa, bool rb, int ob, int wb,
+                                            int lane, const double *vec, double &sa, double &sb) {
+  const int so = V.hd()->soff[r] + lane;
+  const double *rv = V.resv() + so;
+  const uint16_t *rc = V.resc() + so;
+  const double *gv = V.gval(r) + lane;
+  const uint16_t *gc = V.gcol(r) + lane;
+  if (ra && (rb || wb == 0))
+    dot2<true, true>(rv + oa, rc + oa, wa, rv + ob, rc + ob, wb, vec, sa, sb);
+  else if (ra)
+    dot2<true, false>(rv + oa, rc + oa, wa, gv + ob, gc + ob, wb, vec, sa, sb);
+  else
+    dot2<false, false>(gv + oa, gc + oa, wa, gv + ob, gc + ob, wb, vec, sa, sb);
 }
 
 // Phase A: the row sums of one operator application into rs (X rows: P w1
-// +- A' (D Pi) w2 ; Y rows: A w1), slices claimed one at a time from cnt.
+// +- A' (D Pi) w2 ; Y rows: A w1).  Warp w takes slices w, w + nw, ...,
+// two per round when both are on the same side (their loads overlap).
 template <int KIND>
-__device__ __forceinline__ void eng_spmv(const Mats &M, const EngArgs &a, const EngShared &S, int n, const double *in,
-                                         const double *dp, double *rs, const double *sv, const uint16_t *sc,
-                                         int *cnt) {
-  const int lane = threadIdx.x & 31;
-  const Region &RP = S.reg[0], &RT = S.reg[1], &RA = S.reg[2];
-  const int nxs = RP.s1 - RP.s0, ntot = nxs + (RA.s1 - RA.s0);
+__device__ __forceinline__ void eng_spmv(const EngView &V, int n, const double *in, const double *dp, double *rs) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  const int nxs = V.hd()->nxs, ntot = nxs + V.hd()->nys;
   const double *x2 = KIND == STEP_F ? dp : in + n;  // A' gathers D Pi w_2 (F) or w_2 (F')
-  while (true) {
-    int q = 0;
-    if (lane == 0) q = atomicAdd(cnt, 1);
-    q = __shfl_sync(0xffffffffu, q, 0);
-    if (q >= ntot) break;
-    if (q < nxs) {
-      const int s = RP.s0 + q;
-      const double a1 = slice_dot<QG_ENG_UNROLL>(RP, M.sP, a.c16P, s, lane, in, sv, sc);
-      const double a2 = slice_dot<QG_ENG_UNROLL>(RT, M.sAT, a.c16AT, s, lane, x2, sv, sc);
-      const uint16_t r = a.r16x[(int64_t)s * 32 + lane];
-      if (r != kPad16) rs[r] = KIND == STEP_F ? (a1 + a2) : (a1 - a2);
-    } else {
-      const int s = RA.s0 + (q - nxs);
-      const double a1 = slice_dot<QG_ENG_UNROLL>(RA, M.sA, a.c16A, s, lane, in, sv, sc);
-      const uint16_t r = a.r16y[(int64_t)s * 32 + lane];
-      if (r != kPad16) rs[n + r] = a1;
+  for (int qa0 = warp; qa0 < ntot; qa0 += 2 * nw) {
+    int qa = qa0, qb = qa0 + nw;
+    if (qb < ntot && (qa < nxs) != (qb < nxs)) qb = ntot + 1;  // X / Y boundary: one at a time
+    for (int rep = 0; rep < 2; ++rep) {
+      const bool two = qb < ntot;
+      const SliceMeta ma = V.sl()[qa], mb = two ? V.sl()[qb] : ma;
+      double sa, sb;
+      if (qa < nxs) {
+        double ta, tb;
+        region_dot2(V, 0, qa < V.hd()->res[0], ma.off0, ma.w0, !two || qb < V.hd()->res[0], mb.off0,
+                                   two ? mb.w0 : 0, lane, in, sa, sb);
+        region_dot2(V, 1, qa < V.hd()->res[1], ma.off1, ma.w1, !two || qb < V.hd()->res[1], mb.off1,
+                                   two ? mb.w1 : 0, lane, x2, ta, tb);
+        sa = KIND == STEP_F ? (sa + ta) : (sa - ta);
+        sb = KIND == STEP_F ? (sb + tb) : (sb - tb);
+      } else {
+        region_dot2(V, 2, qa - nxs < V.hd()->res[2], ma.off1, ma.w1, !two || qb - nxs < V.hd()->res[2],
+                                   mb.off1, two ? mb.w1 : 0, lane, in, sa, sb);
+      }
+      const int ya = qa < nxs ? 0 : n;
+      const uint16_t ra = V.rows()[qa * 32 + lane];
+      if (ra != kPad16) rs[ya + ra] = sa;
+      if (two) {
+        const uint16_t rb = V.rows()[qb * 32 + lane];
+        if (rb != kPad16) rs[ya + rb] = sb;
+      }
+      // the boundary case: the second slice on its own
+      if (qb == ntot + 1 && qa0 + nw < ntot && rep == 0) {
+        qa = qa0 + nw;
+        qb = ntot;
+      } else {
+        break;
+      }
     }
   }
+}
+
+// Slots of the step partials each application actually fills (X 0..3,
+// Y 4..7): F: P xbar'w, q'w, ||o||^2 / b'D Pi w, ||o||^2 ; F': q'w,
+// ||o||^2 / b'w, ||o||^2 ; slot 3 / 7: ||x||^2 of the fused update.
+template <int KIND>
+__device__ __forceinline__ constexpr unsigned slot_mask(bool upd) {
+  return (KIND == STEP_F ? 0x57u : 0x56u) | (upd ? 0x88u : 0u);
+}
+
+__device__ __forceinline__ void warp_partials(double (&v)[2 * kSlots], double *red, unsigned mask) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 2 * kSlots; ++k)
+    if (mask >> k & 1) v[k] = warp_sum(v[k]);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 2 * kSlots; ++k) red[warp * 2 * kSlots + k] = (mask >> k & 1) ? v[k] : 0.0;
 }
 
 // Warp 0: fixed-order sums of the per-warp partials (lanes 0..7 one slot
@@ -198,39 +337,32 @@ __device__ __forceinline__ void warp0_sums(const double *red, double (&s)[2 * kS
   for (int k = 0; k < 2 * kSlots; ++k) s[k] = __shfl_sync(0xffffffffu, t, k);
 }
 
-__device__ __forceinline__ void warp_partials(double (&v)[2 * kSlots], double *red) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < 2 * kSlots; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < 2 * kSlots; ++k) red[warp * 2 * kSlots + k] = v[k];
-}
-
 struct Geo {
   int n, m;
   int64_t xo, yo, T;
-  int yu0, yu1;  // Y work units (cone-block classes)
 };
 
 // Phase B: row epilogue of one application (graph path expressions,
 // operator.cu step_unit): out <- s_in OP(in) - c_out out (in place), with
 // the deferred LSMR vector update fused into the u-step (upd), per-warp
-// partials into red (X slots 0..3, Y slots 4..7; slot 3 / 7: ||x||^2).
+// partials into red.  z_N = 1 (every jvp / vjp) skips the divisions.
 template <int KIND>
-__device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, const Geo &g, const Embed &E,
-                                             const double *in, double *out, const double *rs, double *rsw,
+__device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, const EngView &V, const Geo &g,
+                                             const Embed &E, const double *in, double *out, double *rs,
                                              double *dp, double s_in, double c_out, bool upd, const Lsmr &L,
                                              double *red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nt = (int)blockDim.x, nw = nt >> 5;
   const int n = g.n, m = g.m;
-  const int by = (int)g.yo;
   const double wN = in[n + m];
+  const bool zn1 = E.zN == 1.0;
+  const double zN = E.zN;
+  auto divz = [&](double x) { return zn1 ? x : x / zN; };
   double acc[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
   if (upd) {
     // hbar = h - c1 hbar ; x = x + c2 hbar ; h = v s_v - c3 h (v = this step's input)
     const double c1 = L.c_hbar, c2 = L.c_x, c3 = L.c_h, svs = L.s_v;
-    for (int i = tid; i < n + m; i += (int)blockDim.x) {
+    for (int i = tid; i < n + m; i += nt) {
       const int64_t gi = i < n ? g.xo + i : M.NX + g.yo + (i - n);
       const double hv = __ldcg(a.h + gi), hbo = __ldcg(a.hb + gi), xo = __ldcg(a.x + gi);
       const double hbv = hv - c1 * hbo;
@@ -241,67 +373,65 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
       if (i < n) acc[3] += xv * xv; else acc[7] += xv * xv;
     }
   }
-  const double izN = E.zN;
-  for (int i = tid; i < n; i += (int)blockDim.x) {
+  for (int i = tid; i < n; i += nt) {
     const int64_t r = g.xo + i;
-    const double w = in[i];
+    const double w = in[i], qr = M.q[r], px = M.Pxbar[r];
     double res;
     if (KIND == STEP_F) {
-      const double o1 = rs[i] + wN * M.q[r];
-      res = ((o1 - w) + w) / izN;
-      acc[0] += M.Pxbar[r] * w;
+      const double o1 = rs[i] + wN * qr;
+      res = divz((o1 - w) + w);
+      acc[0] += px * w;
     } else {
-      const double gg = (rs[i] - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
-      res = ((gg - w) + w) / izN;
+      const double gg = (rs[i] - ((2.0 / E.tau) * wN) * px) - wN * qr;
+      res = divz((gg - w) + w);
     }
-    acc[1] += M.q[r] * w;
+    acc[1] += qr * w;
     const double o = s_in * res - (c_out != 0.0 ? c_out * out[i] : 0.0);
     out[i] = o;
     acc[2] += o * o;
   }
   double *outY = out + n;
   const double *inY = in + n;
+  const double *bY = M.b + g.yo, *zY = M.dpi.zmid + g.yo;
   if (KIND == STEP_F) {
-    for (int j = tid; j < m; j += (int)blockDim.x) {
-      const int64_t r = g.yo + j;
-      const double o2 = (-rs[n + j]) + wN * M.b[r];
-      const double res = ((o2 - dp[j]) + inY[j]) / izN;
+    for (int j = tid; j < m; j += nt) {
+      const double br = bY[j];
+      const double o2 = (-rs[n + j]) + wN * br;
+      const double res = divz((o2 - dp[j]) + inY[j]);
       const double o = s_in * res - (c_out != 0.0 ? c_out * outY[j] : 0.0);
       outY[j] = o;
-      acc[4] += M.b[r] * dp[j];
+      acc[4] += br * dp[j];
       acc[6] += o * o;
     }
   } else {
-    // t = (A w1 - w_N b) - w2 (recomputed where needed), then per cone block:
+    // t = (A w1 - w_N b) - w2, then per cone block:
     // o = s_in (D Pi t + w2)/z_N - c_out old ; dp = D Pi o
-    const double *tsrc = rs + n;
-    auto tval = [&](int j) { return (tsrc[j] - wN * M.b[g.yo + j]) - inY[j]; };
+    auto tval = [&](int j) { return (rs[n + j] - wN * bY[j]) - inY[j]; };
     auto fin_row = [&](int j, double dpt) {
       const double w = inY[j];
-      const double o = s_in * ((dpt + w) / izN) - (c_out != 0.0 ? c_out * outY[j] : 0.0);
+      const double o = s_in * divz(dpt + w) - (c_out != 0.0 ? c_out * outY[j] : 0.0);
       outY[j] = o;
-      acc[4] += M.b[g.yo + j] * w;
+      acc[4] += bY[j] * w;
       acc[6] += o * o;
       return o;
     };
     const DpiView &dv = M.dpi;
-    for (int ui = g.yu0; ui < g.yu1; ++ui) {
-      const Unit u = M.yu[ui];
+    const int nyu = V.hd()->nyu;
+    for (int ui = 0; ui < nyu; ++ui) {
+      const EUnit u = V.units()[ui];
       if (u.cls == CLS_ELEM) {
-        const int kind = dv.blk[u.blk0].kind;
-        for (int r = u.row0 + tid; r < u.row1; r += (int)blockDim.x) {
-          const int j = r - by;
-          const double wgt = elem_weight(kind, dv.dual, dv.zmid[r]);
+        for (int j = u.row0 + tid; j < u.row1; j += nt) {
+          const double wgt = elem_weight(u.kind, dv.dual, zY[j]);
           const double o = fin_row(j, wgt * tval(j));
           dp[j] = wgt * o;
         }
       } else if (u.cls == CLS_TRI) {
-        for (int k = u.blk0 + tid; k < u.blk1; k += (int)blockDim.x) {
-          const BlockInfo b = dv.blk[k];
-          const int j = b.row - by;
+        for (int k = u.blk0 + tid; k < u.blk1; k += nt) {
+          const EBlk b = V.blks()[k];
+          const int j = b.j0;
           double D[9];
 #pragma unroll
-          for (int i = 0; i < 9; ++i) D[i] = dv.tri_D[9 * b.param + i];
+          for (int i = 0; i < 9; ++i) D[i] = dv.tri_D[9 * (int64_t)b.param + i];
           const int flip = dv.tri_flip[b.param];
           const double t3[3] = {tval(j), tval(j + 1), tval(j + 2)};
           double r3[3], o3[3], d3[3];
@@ -312,22 +442,21 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
 #pragma unroll
           for (int i = 0; i < 3; ++i) dp[j + i] = d3[i];
         }
-      } else if (u.cls == CLS_SOC && u.group > 0) {
-        // G = u.group lanes per block (dims <= 32), one lane per row:
-        // soc_entry twice (cones.py:740-764) with group shuffle sums
-        const int G = u.group, per = 32 / G, lg = lane & (G - 1);
-        const int nw = (int)(blockDim.x >> 5);
+      } else if (u.G > 0) {
+        // G lanes per SOC block (dims <= 32), one lane per row: soc_entry
+        // twice (cones.py:740-764) with group shuffle sums
+        const int G = u.G, per = 32 / G, lg = lane & (G - 1), src = lane & ~(G - 1);
         for (int base = u.blk0 + warp * per; base < u.blk1; base += nw * per) {
           const int k = base + lane / G;
-          const bool blk_ok = k < u.blk1;
-          const BlockInfo b = dv.blk[blk_ok ? k : u.blk0];
-          const int dim = blk_ok ? b.dim : 0, j0 = b.row - by, code = dv.soc_code[b.param];
+          const bool kok = k < u.blk1;
+          const EBlk b = V.blks()[kok ? k : u.blk0];
+          const int dim = kok ? b.dim : 0, j0 = b.j0;
+          const int code = dv.soc_code[b.param];
           const double nu = dv.soc_nu[b.param];
           const bool ok = lg < dim;
-          const double zi = ok ? dv.zmid[b.row + lg] : 0.0;
+          const double zi = ok ? zY[j0 + lg] : 0.0;
           const double ti = ok ? tval(j0 + lg) : 0.0;
           const double udu = gsum((ok && lg > 0) ? zi * ti : 0.0, G);
-          const int src = lane & ~(G - 1);
           const double t0 = __shfl_sync(0xffffffffu, zi, src), dt = __shfl_sync(0xffffffffu, ti, src);
           const double oi = ok ? fin_row(j0 + lg, soc_entry(code, lg, nu, t0, zi, ti, dt, udu)) : 0.0;
           const double udu2 = gsum((ok && lg > 0) ? zi * oi : 0.0, G);
@@ -336,137 +465,122 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
         }
       } else {
         // large SOC blocks: a warp per block (soc_apply_warp), t in place in rs
-        for (int k = u.blk0 + warp; k < u.blk1; k += (int)(blockDim.x >> 5)) {
-          const BlockInfo b = dv.blk[k];
-          const int dim = b.dim, j0 = b.row - by;
-          double *tb = rsw + n + j0;
+        for (int k = u.blk0 + warp; k < u.blk1; k += nw) {
+          const EBlk b = V.blks()[k];
+          const int dim = b.dim, j0 = b.j0;
+          const int code = dv.soc_code[b.param];
+          const double nu = dv.soc_nu[b.param];
+          double *tb = rs + n + j0;
           for (int i = lane; i < dim; i += 32) tb[i] = tval(j0 + i);
           __syncwarp();
-          soc_apply_warp(dv.zmid + b.row, dim, dv.soc_nu[b.param], dv.soc_code[b.param], tb, tb);
+          soc_apply_warp(zY + j0, dim, nu, code, tb, tb);
           __syncwarp();
           for (int i = lane; i < dim; i += 32) fin_row(j0 + i, tb[i]);
           __syncwarp();
-          soc_apply_warp(dv.zmid + b.row, dim, dv.soc_nu[b.param], dv.soc_code[b.param], outY + j0, dp + j0);
+          soc_apply_warp(zY + j0, dim, nu, code, outY + j0, dp + j0);
           __syncwarp();
         }
       }
     }
   }
-  warp_partials(acc, red);
+  warp_partials(acc, red, slot_mask<KIND>(upd));
 }
 
-// Resident prefix of one region: the largest slice prefix whose entries fit
-// in `room` (counted by the whole CTA; S.off is monotone).
-__device__ __forceinline__ void plan_region(Region &R, const SellView &S, int s0, int s1, int &room, int &soff,
-                                            int *count) {
-  const int64_t g0 = S.off[s0];
-  int c = 0;
-  for (int s = s0 + (int)threadIdx.x; s < s1; s += (int)blockDim.x) c += (S.off[s + 1] - g0 <= room) ? 1 : 0;
-  if (threadIdx.x == 0) *count = 0;
-  __syncthreads();
-  if (c) atomicAdd(count, c);
-  __syncthreads();
-  const int sres = s0 + *count;
-  const int ent = (int)(S.off[sres] - g0);
-  if (threadIdx.x == 0) {
-    R.g0 = g0;
-    R.s0 = s0;
-    R.s1 = s1;
-    R.sres = sres;
-    R.soff = soff;
-  }
-  room -= ent;
-  soff += ent;
-  __syncthreads();
-}
-
-template <int KU, int KV, int NT>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_engine(Mats M, EngArgs a) {
+template <int KU, int KV, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ EngShared S;
   Lsmr &L = *reinterpret_cast<Lsmr *>(S.L);
   constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double *su = sm, *sv = sm + a.nmax, *rs = sm + 2 * a.nmax, *dp = sm + 3 * a.nmax;
-  double *resv = sm + a.vec_doubles;                                  // resident values (16-byte aligned)
-  uint16_t *resc = reinterpret_cast<uint16_t *>(resv + a.res_cap);   // resident 16-bit columns
-  if (tid == 0) mbar_init(&S.mbar, 1);
+  const EngView V{M, a};
+  unsigned char *blob = V.blob();  // 16-byte aligned
+  double *resv = V.resv();
+  uint16_t *resc = V.resc();
+  if (tid == 0) {
+    mbar_init(&S.mbar, 1);
+    for (int k = 0; k < 8; ++k) S.prof[k] = 0;
+  }
   __syncthreads();
   uint32_t mphase = 0;
+  const bool prof = a.prof != nullptr && tid == 0;
+  long long t_mark = 0;
+  auto tick = [&](int k) {
+    if (prof) {
+      const long long t = clock64();
+      S.prof[k] += (unsigned long long)(t - t_mark);
+      t_mark = t;
+    }
+  };
 
   while (true) {
     if (tid == 0) S.p = atomicAdd(a.next, 1);
     __syncthreads();
     const int p = S.p;
-    if (p >= a.B) return;
+    if (p >= a.B) {
+      if (prof)
+        for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, S.prof[k]);
+      return;
+    }
+    if (prof) t_mark = clock64();
     Geo g;
     g.xo = M.xoff[p];
     g.yo = M.yoff[p];
     g.n = (int)(M.xoff[p + 1] - g.xo);
     g.m = (int)(M.yoff[p + 1] - g.yo);
     g.T = M.NX + M.NY + p;
-    const int64_t xu0 = M.xu_ptr[p], xu1 = M.xu_ptr[p + 1], yu0 = M.yu_ptr[p], yu1 = M.yu_ptr[p + 1];
-    g.yu0 = (int)yu0;
-    g.yu1 = (int)yu1;
-    const int xs0 = xu1 > xu0 ? M.xu[xu0].s0 : 0, xs1 = xu1 > xu0 ? M.xu[xu1 - 1].s1 : 0;
-    const int ys0 = yu1 > yu0 ? M.yu[yu0].s0 : 0, ys1 = yu1 > yu0 ? M.yu[yu1 - 1].s1 : 0;
     const int n = g.n, m = g.m, nm = n + m;
     const Embed E = M.emb[p];
-    // resident slice prefixes: P, then A (Y), then A' with what is left
-    {
-      int room = a.res_cap, soff = 0;
-      plan_region(S.reg[0], M.sP, xs0, xs1, room, soff, &S.rescount);
-      plan_region(S.reg[2], M.sA, ys0, ys1, room, soff, &S.rescount);
-      plan_region(S.reg[1], M.sAT, xs0, xs1, room, soff, &S.rescount);
-    }
+    const unsigned char *gblob = a.blob + (size_t)p * a.bl.stride;
+    const EngHead *gh = reinterpret_cast<const EngHead *>(gblob);
+    const SellView *mats[3] = {&M.sP, &M.sAT, &M.sA};
+    const uint16_t *c16[3] = {a.c16P, a.c16AT, a.c16A};
     if (tid == 0) {
-      // one mbarrier phase per problem: every resident region by bulk copies
-      // (all offsets are multiples of 32 entries: 16-byte aligned both sides)
+      // one mbarrier phase per problem: the meta blob and every resident
+      // region by bulk copies (all sizes / offsets multiples of 16 bytes)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the area
-      uint32_t bytes = 0;
-      const SellView *mats[3] = {&M.sP, &M.sAT, &M.sA};
-      const uint16_t *c16[3] = {a.c16P, a.c16AT, a.c16A};
-      for (int r = 0; r < 3; ++r) {
-        const Region &R = S.reg[r];
-        bytes += (uint32_t)(mats[r]->off[R.sres] - R.g0) * 10u;
-      }
+      const EngHead h = *gh;
+      uint32_t bytes = (uint32_t)a.bl.stride;
+      for (int r = 0; r < 3; ++r) bytes += (uint32_t)h.ent[r] * 10u;
       mbar_expect_tx(&S.mbar, bytes);
-      for (int r = 0; r < 3; ++r) {
-        const Region &R = S.reg[r];
-        const uint32_t ent = (uint32_t)(mats[r]->off[R.sres] - R.g0);
-        if (ent) {
-          bulk_g2s(resv + R.soff, mats[r]->val + R.g0, ent * 8u, &S.mbar);
-          bulk_g2s(resc + R.soff, c16[r] + R.g0, ent * 2u, &S.mbar);
+      bulk_g2s(blob, gblob, (uint32_t)a.bl.stride, &S.mbar);
+      for (int r = 0; r < 3; ++r)
+        if (h.ent[r]) {
+          bulk_g2s(resv + h.soff[r], mats[r]->val + h.g0[r], (uint32_t)h.ent[r] * 8u, &S.mbar);
+          bulk_g2s(resc + h.soff[r], c16[r] + h.g0[r], (uint32_t)h.ent[r] * 2u, &S.mbar);
         }
-      }
     }
     // LSMR state, u, v (rows + T), D Pi of the F input, T entries of h / hbar / x
     const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(a.st + p);
-    for (int w = tid; w < kLw; w += (int)blockDim.x) S.L[w] = Lg[w];
-    for (int i = tid; i < nm; i += (int)blockDim.x) {
+    for (int w = tid; w < kLw; w += NT) S.L[w] = Lg[w];
+    for (int i = tid; i < nm; i += NT) {
       const int64_t gi = i < n ? g.xo + i : M.NX + g.yo + (i - n);
       su[i] = a.u[gi];
       sv[i] = a.v[gi];
     }
     if (a.dp0)
-      for (int j = tid; j < m; j += (int)blockDim.x) dp[j] = a.dp0[g.yo + j];
+      for (int j = tid; j < m; j += NT) dp[j] = a.dp0[g.yo + j];
     if (tid == 0) {
       su[nm] = a.u[g.T];
       sv[nm] = a.v[g.T];
       S.tvh[0] = a.h[g.T];
       S.tvh[1] = a.hb[g.T];
       S.tvh[2] = a.x[g.T];
-      S.cnt[0] = S.cnt[1] = 0;
     }
     mbar_wait(&S.mbar, mphase);
     mphase ^= 1;
     __syncthreads();
+    tick(0);
 
     bool pending_v = false;  // a v-step's partials await fin V (warp 0, during A_u)
     if (L.active) {
       while (true) {
         // ---- A_u || fin V of the previous iteration
+        const bool prof1 = a.prof != nullptr && tid == 32;
+        long long t_sp = prof1 ? clock64() : 0;
         if (warp == 0 && pending_v) {
+          const long long t_f = prof ? clock64() : 0;
           double s8[2 * kSlots];
           warp0_sums(S.red, s8);
           if (lane == 0) {
@@ -476,45 +590,54 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_engine(Mats M, EngArgs a) {
             if (w & TV_H) S.tvh[0] = t.h;
             if (w & TV_HB) S.tvh[1] = t.hb;
             if (w & TV_X) S.tvh[2] = t.x;
+            if (prof) S.prof[6] += (unsigned long long)(clock64() - t_f);
           }
           __syncwarp();
         }
-        eng_spmv<KU>(M, a, S, n, sv, dp, rs, resv, resc, &S.cnt[0]);
+        eng_spmv<KU>(V, n, sv, dp, rs);
+        if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
+        tick(1);
         if (!L.active) break;  // fin V stopped the solve (non-finite)
         // ---- B_u (+ the deferred update of the previous iteration)
-        if (tid == 0) S.cnt[1] = 0;
-        eng_epilogue<KU>(M, a, g, E, sv, su, rs, rs, dp, L.s_in, L.c_out, L.itn > 0, L, S.red);
+        eng_epilogue<KU>(M, a, V, g, E, sv, su, rs, dp, L.s_in, L.c_out, L.itn > 0, L, S.red);
         __syncthreads();
+        tick(2);
         // ---- A_v || stop test + fin U
+        if (prof1) t_sp = clock64();
         if (warp == 0) {
+          const long long t_f = prof ? clock64() : 0;
           double s8[2 * kSlots];
           warp0_sums(S.red, s8);
           if (lane == 0) {
-            bool stop = L.itn > 0 && stop_test(&L, s8[3] + s8[kSlots + 3], S.tvh[2]);
+            const bool stop = L.itn > 0 && stop_test(&L, s8[3] + s8[kSlots + 3], S.tvh[2]);
             if (!stop) {
               TVals t{sv[nm], su[nm], su[nm], S.tvh[0], S.tvh[1], S.tvh[2], 0.0};
               const int w = fin_core(E, PH_STEP_U, KU, &L, s8, s8 + kSlots, t, false, false);
               if (w & TV_OUT) su[nm] = t.out;
             }
+            if (prof) S.prof[6] += (unsigned long long)(clock64() - t_f);
           }
           __syncwarp();
         }
-        eng_spmv<KV>(M, a, S, n, su, dp, rs, resv, resc, &S.cnt[1]);
+        eng_spmv<KV>(V, n, su, dp, rs);
+        if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
+        tick(3);
         if (!L.active) break;  // the stop test ended the solve
         // ---- B_v (a zero beta skips the v-step: fin V keeps v)
-        if (tid == 0) S.cnt[0] = 0;
-        if (!L.skip_v) eng_epilogue<KV>(M, a, g, E, su, sv, rs, rs, dp, L.s_in, L.c_out, false, L, S.red);
+        if (!L.skip_v) eng_epilogue<KV>(M, a, V, g, E, su, sv, rs, dp, L.s_in, L.c_out, false, L, S.red);
         pending_v = true;
         __syncthreads();
+        tick(4);
+        if (prof) S.prof[5] += 1;
       }
     }
 
     // write back: state, T entries, u and v (x / h / hbar rows are global)
     unsigned long long *Lw = reinterpret_cast<unsigned long long *>(a.st + p);
-    for (int w = tid; w < kLw; w += (int)blockDim.x) Lw[w] = S.L[w];
-    for (int i = tid; i < nm; i += (int)blockDim.x) {
+    for (int w = tid; w < kLw; w += NT) Lw[w] = S.L[w];
+    for (int i = tid; i < nm; i += NT) {
       const int64_t gi = i < n ? g.xo + i : M.NX + g.yo + (i - n);
       a.u[gi] = su[i];
       a.v[gi] = sv[i];
@@ -530,22 +653,94 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_engine(Mats M, EngArgs a) {
   }
 }
 
-// ------------------------------------------------- 16-bit local indices --
-// Warp per slice: local column (col - the problem's column base) and local
-// row of every entry / lane of a SELL matrix.
+// ------------------------------------------------- engine preparation --
+// Warp per slice: local column (col - the problem's column base) of every
+// entry of a SELL matrix.
 __global__ void k_local16(int64_t nslices, const int32_t *sprob, const int64_t *off, const int32_t *w,
-                          const int32_t *col, const int64_t *cbase, uint16_t *c16, const int32_t *rowof,
-                          const int64_t *rbase, uint16_t *r16) {
+                          const int32_t *col, const int64_t *cbase, uint16_t *c16) {
   const int64_t s = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (s >= nslices) return;
-  const int p = sprob[s];
-  const int64_t cb = cbase[p];
+  const int64_t cb = cbase[sprob[s]];
   const int64_t o = off[s];
   for (int k = 0; k < w[s]; ++k) c16[o + 32LL * k + lane] = (uint16_t)(col[o + 32LL * k + lane] - cb);
-  if (r16) {
-    const int r = rowof[s * 32 + lane];
-    r16[s * 32 + lane] = r >= 0 ? (uint16_t)(r - rbase[p]) : kPad16;
+}
+
+// One CTA per problem: its meta blob (slice table, local rows, Y units,
+// blocks) and the resident plan (largest slice prefix of P, then A', then A
+// fitting res_cap entries).
+__global__ void k_engine_meta(Mats M, BlobLayout bl, int res_cap, unsigned char *blobs) {
+  const int p = blockIdx.x;
+  unsigned char *b = blobs + (size_t)p * bl.stride;
+  EngHead *hd = reinterpret_cast<EngHead *>(b);
+  SliceMeta *sl = reinterpret_cast<SliceMeta *>(b + bl.o_slices);
+  uint16_t *rows = reinterpret_cast<uint16_t *>(b + bl.o_rows);
+  EUnit *un = reinterpret_cast<EUnit *>(b + bl.o_units);
+  EBlk *bk = reinterpret_cast<EBlk *>(b + bl.o_blks);
+  const int64_t xu0 = M.xu_ptr[p], xu1 = M.xu_ptr[p + 1], yu0 = M.yu_ptr[p], yu1 = M.yu_ptr[p + 1];
+  const int xs0 = xu1 > xu0 ? M.xu[xu0].s0 : 0, xs1 = xu1 > xu0 ? M.xu[xu1 - 1].s1 : 0;
+  const int ys0 = yu1 > yu0 ? M.yu[yu0].s0 : 0, ys1 = yu1 > yu0 ? M.yu[yu1 - 1].s1 : 0;
+  const int kb0 = yu1 > yu0 ? M.yu[yu0].blk0 : 0, kb1 = yu1 > yu0 ? M.yu[yu1 - 1].blk1 : 0;
+  const int nxs = xs1 - xs0, nys = ys1 - ys0;
+  const int64_t xo = M.xoff[p], yo = M.yoff[p];
+  const int64_t g0[3] = {M.sP.off[xs0], M.sAT.off[xs0], M.sA.off[ys0]};
+  for (int q = threadIdx.x; q < nxs + nys; q += blockDim.x) {
+    SliceMeta s{};
+    if (q < nxs) {
+      const int gs = xs0 + q;
+      s.off0 = (int32_t)(M.sP.off[gs] - g0[0]);
+      s.off1 = (int32_t)(M.sAT.off[gs] - g0[1]);
+      s.w0 = (uint16_t)M.sP.w[gs];
+      s.w1 = (uint16_t)M.sAT.w[gs];
+    } else {
+      const int gs = ys0 + (q - nxs);
+      s.off1 = (int32_t)(M.sA.off[gs] - g0[2]);
+      s.w1 = (uint16_t)M.sA.w[gs];
+    }
+    sl[q] = s;
+  }
+  for (int i = threadIdx.x; i < 32 * (nxs + nys); i += blockDim.x) {
+    const int q = i / 32, lane = i % 32;
+    const int r = q < nxs ? M.x_rowof[(int64_t)(xs0 + q) * 32 + lane] : M.y_rowof[(int64_t)(ys0 + q - nxs) * 32 + lane];
+    rows[i] = r < 0 ? kPad16 : (uint16_t)(r - (q < nxs ? xo : yo));
+  }
+  for (int ui = (int)yu0 + threadIdx.x; ui < (int)yu1; ui += blockDim.x) {
+    const Unit u = M.yu[ui];
+    EUnit e{};
+    e.cls = u.cls;
+    e.kind = M.dpi.blk[u.blk0].kind;
+    e.G = u.cls == CLS_SOC ? u.group : 0;
+    e.row0 = (int32_t)(u.row0 - yo);
+    e.row1 = (int32_t)(u.row1 - yo);
+    e.blk0 = u.blk0 - kb0;
+    e.blk1 = u.blk1 - kb0;
+    un[ui - yu0] = e;
+  }
+  for (int k = kb0 + threadIdx.x; k < kb1; k += blockDim.x) {
+    const BlockInfo bi = M.dpi.blk[k];
+    bk[k - kb0] = EBlk{(int32_t)bi.param, (uint16_t)(bi.row - yo), (uint16_t)bi.dim};
+  }
+  if (threadIdx.x == 0) {
+    EngHead h{};
+    h.nxs = nxs;
+    h.nys = nys;
+    h.nyu = (int)(yu1 - yu0);
+    h.nblk = kb1 - kb0;
+    const SellView *mats[3] = {&M.sP, &M.sAT, &M.sA};
+    const int sr0[3] = {xs0, xs0, ys0}, sr1[3] = {xs1, xs1, ys1};
+    int room = res_cap, soff = 0;
+    for (int r : {0, 1, 2}) {  // P, then A' (wide X rows), then A: the streamed rest are narrow Y slices
+      int s = sr0[r];
+      while (s < sr1[r] && mats[r]->off[s + 1] - g0[r] <= room) ++s;
+      const int ent = (int)(mats[r]->off[s] - g0[r]);
+      h.res[r] = s - sr0[r];
+      h.soff[r] = soff;
+      h.ent[r] = ent;
+      h.g0[r] = g0[r];
+      room -= ent;
+      soff += ent;
+    }
+    *hd = h;
   }
 }
 
@@ -558,9 +753,8 @@ static void engine_dims(const Handle &H, int &nmax, int &mmax) {
   }
 }
 
-constexpr size_t kEngSmemMax = 227 * 1024 - sizeof(EngShared) - 256;        // one CTA per SM
+constexpr size_t kEngSmemMax = 227 * 1024 - sizeof(EngShared) - 256;              // one CTA per SM
 constexpr size_t kEngSmemMax2 = 228 * 1024 / 2 - 1024 - sizeof(EngShared) - 256;  // two CTAs per SM
-constexpr size_t kEngMinResident = 0;
 
 static size_t engine_vec_bytes(const Handle &H) {
   int nmax, mmax;
@@ -568,13 +762,49 @@ static size_t engine_vec_bytes(const Handle &H) {
   return sizeof(double) * (size_t)((3 * nmax + mmax + 1) & ~1);
 }
 
+// CTA shape (QG_ENG_CFG, A/B): 1 (default) = 512 threads with 128
+// registers, one CTA per SM (c5a loop 85.6 ms per solve, c1 1.3 ms per 148
+// problems); 0 = 1024 threads at 64 registers (spills in the finalize: 89 /
+// 2.0 ms); 2 = 512 threads, two CTAs (problems) per SM with a third of the
+// resident matrix each (96 ms).
+static int engine_cfg() {
+  static const char *env = std::getenv("QG_ENG_CFG");
+  static const int c = env ? std::max(0, std::min(2, std::atoi(env))) : 1;
+  return c;
+}
+static int engine_threads() { return engine_cfg() == 0 ? 1024 : 512; }
+static int engine_ctas_per_sm() { return engine_cfg() == 2 ? 2 : 1; }
+
+// Blob maxima from the host-side units / blocks (slices: the unit ranges).
+static BlobLayout engine_blob_layout(const Handle &H) {
+  int smax = 0, umax = 0, bmax = 0;
+  for (int p = 0; p < H.B; ++p) {
+    int ns = 0;
+    for (int64_t u = H.xunit_ptr[p]; u < H.xunit_ptr[p + 1]; ++u) ns += H.xunits[u].s1 - H.xunits[u].s0;
+    const int64_t y0 = H.cones.unit_ptr[p], y1 = H.cones.unit_ptr[p + 1];
+    for (int64_t u = y0; u < y1; ++u) ns += H.cones.units[u].s1 - H.cones.units[u].s0;
+    smax = std::max(smax, ns);
+    umax = std::max(umax, (int)(y1 - y0));
+    if (y1 > y0) bmax = std::max(bmax, H.cones.units[y1 - 1].blk1 - H.cones.units[y0].blk0);
+  }
+  return blob_layout(smax, umax, bmax);
+}
+
+static int engine_res_cap(const Handle &H, size_t blob_stride) {
+  const size_t cap = engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax;
+  const size_t used = engine_vec_bytes(H) + blob_stride;
+  int rc = used < cap ? (int)(((cap - used) / 10) & ~size_t(31)) : 0;
+  if (const char *e = std::getenv("QG_ENG_RESIDENT")) rc = std::min(rc, std::atoi(e) & ~31);  // A/B
+  return rc;
+}
+
 bool engine_candidate(const Handle &H) {
   if (H.comm || H.cones.max_psd_order > 0) return false;
   const char *env = std::getenv("QG_ENGINE");
   if (env && std::atoi(env) == 0) return false;
-  if (engine_vec_bytes(H) + kEngMinResident > kEngSmemMax) return false;
   for (int p = 0; p < H.B; ++p)
     if (H.n[p] >= 65535 || H.m[p] >= 65535) return false;  // 16-bit local indices
+  if (engine_vec_bytes(H) + 16 * 1024 > (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax)) return false;
   if (env && std::atoi(env) != 0) return true;
   // resident solves win when the batch fills the GPU with problems, or the
   // single problems are small enough that launch latency dominates
@@ -587,7 +817,8 @@ bool engine_units_ok(const Handle &H) {
   for (const auto *us : {&H.xunits, &H.cones.units})
     for (const Unit &u : *us)
       if (u.mode != MODE_SELL) return false;
-  return true;
+  const BlobLayout bl = engine_blob_layout(H);
+  return engine_vec_bytes(H) + bl.stride <= (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax);
 }
 
 static void slice_probs(const std::vector<Unit> &units, int64_t nslices, std::vector<int32_t> &out) {
@@ -596,6 +827,8 @@ static void slice_probs(const std::vector<Unit> &units, int64_t nslices, std::ve
     for (int s = u.s0; s < u.s1; ++s) out[s] = u.prob;
 }
 
+// After build_sell (slices) and the cone table: 16-bit local columns and
+// the per-problem meta blobs.
 void build_engine_layout(Handle &H, cudaStream_t st) {
   std::vector<int32_t> spx, spy;
   slice_probs(H.xunits, H.nslice_x, spx);
@@ -606,22 +839,24 @@ void build_engine_layout(Handle &H, cudaStream_t st) {
   H.c16P = dev_alloc<uint16_t>(H.sP.entries);
   H.c16AT = dev_alloc<uint16_t>(H.sAT.entries);
   H.c16A = dev_alloc<uint16_t>(H.sA.entries);
-  H.r16x = dev_alloc<uint16_t>(32 * std::max<int64_t>(H.nslice_x, 1));
-  H.r16y = dev_alloc<uint16_t>(32 * std::max<int64_t>(H.nslice_y, 1));
   const unsigned gx = (unsigned)((H.nslice_x * 32 + 255) / 256), gy = (unsigned)((H.nslice_y * 32 + 255) / 256);
   if (H.nslice_x) {
-    k_local16<<<gx, 256, 0, st>>>(H.nslice_x, d_spx, H.sP.off, H.sP.w, H.sP.col, H.d_xoff, H.c16P, H.x_rowof,
-                                  H.d_xoff, H.r16x);
+    k_local16<<<gx, 256, 0, st>>>(H.nslice_x, d_spx, H.sP.off, H.sP.w, H.sP.col, H.d_xoff, H.c16P);
     QG_LAUNCHED();
-    k_local16<<<gx, 256, 0, st>>>(H.nslice_x, d_spx, H.sAT.off, H.sAT.w, H.sAT.col, H.d_yoff, H.c16AT, nullptr,
-                                  nullptr, nullptr);
+    k_local16<<<gx, 256, 0, st>>>(H.nslice_x, d_spx, H.sAT.off, H.sAT.w, H.sAT.col, H.d_yoff, H.c16AT);
     QG_LAUNCHED();
   }
   if (H.nslice_y) {
-    k_local16<<<gy, 256, 0, st>>>(H.nslice_y, d_spy, H.sA.off, H.sA.w, H.sA.col, H.d_xoff, H.c16A, H.y_rowof,
-                                  H.d_yoff, H.r16y);
+    k_local16<<<gy, 256, 0, st>>>(H.nslice_y, d_spy, H.sA.off, H.sA.w, H.sA.col, H.d_xoff, H.c16A);
     QG_LAUNCHED();
   }
+  const BlobLayout bl = engine_blob_layout(H);
+  H.eng_res_cap = engine_res_cap(H, bl.stride);
+  H.eng_blob = dev_alloc<unsigned char>(bl.stride * (size_t)H.B);
+  QG_CUDA(cudaMemsetAsync(H.eng_blob, 0, bl.stride * (size_t)H.B, st));
+  Mats M = make_mats(H);
+  k_engine_meta<<<H.B, 256, 0, st>>>(M, bl, H.eng_res_cap, H.eng_blob);
+  QG_LAUNCHED();
   QG_CUDA(cudaStreamSynchronize(st));  // host vectors spx / spy
   dev_free(d_spx);
   dev_free(d_spy);
@@ -634,28 +869,43 @@ void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st) {
   a.u = W.u; a.v = W.v; a.h = W.h; a.hb = W.hb; a.x = W.x;
   a.dp0 = jvp ? W.dpv : nullptr;
   a.c16P = H.c16P; a.c16AT = H.c16AT; a.c16A = H.c16A;
-  a.r16x = H.r16x; a.r16y = H.r16y;
+  a.blob = H.eng_blob;
+  a.bl = engine_blob_layout(H);
   a.next = W.d_claim;
   a.B = H.B;
   engine_dims(H, a.nmax, a.mmax);
   a.vec_doubles = (3 * a.nmax + a.mmax + 1) & ~1;
-  const size_t vec = sizeof(double) * (size_t)a.vec_doubles;
-  static const char *env_nt = std::getenv("QG_ENG_THREADS");  // A/B: 512 = two CTAs (problems) per SM
-  const int nt = env_nt && std::atoi(env_nt) == 512 ? 512 : 1024;
-  const size_t cap = nt == 512 ? kEngSmemMax2 : kEngSmemMax;
-  a.res_cap = vec < cap ? (int)(((cap - vec) / 10) & ~size_t(31)) : 0;
-  if (const char *e = std::getenv("QG_ENG_RESIDENT")) a.res_cap = std::min(a.res_cap, std::atoi(e) & ~31);  // A/B
-  const size_t smem = vec + (size_t)a.res_cap * 10;
-  auto kern = nt == 512 ? (jvp ? k_engine<STEP_F, STEP_FT, 512> : k_engine<STEP_FT, STEP_F, 512>)
-                        : (jvp ? k_engine<STEP_F, STEP_FT, 1024> : k_engine<STEP_FT, STEP_F, 1024>);
+  a.res_cap = H.eng_res_cap;
+  const int nt = engine_threads();
+  const size_t smem = sizeof(double) * (size_t)a.vec_doubles + a.bl.stride + (size_t)a.res_cap * 10;
+  const int cfg = engine_cfg();
+  auto kern = cfg == 2 ? (jvp ? k_engine<STEP_F, STEP_FT, 512, 2> : k_engine<STEP_FT, STEP_F, 512, 2>)
+              : cfg == 1 ? (jvp ? k_engine<STEP_F, STEP_FT, 512, 1> : k_engine<STEP_FT, STEP_F, 512, 1>)
+                         : (jvp ? k_engine<STEP_F, STEP_FT, 1024, 1> : k_engine<STEP_FT, STEP_F, 1024, 1>);
   QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, nsm = 0;
   QG_CUDA(cudaGetDevice(&dev));
   QG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-  const int grid = std::max(1, std::min(H.B, nsm * (1024 / nt)));
+  const int grid = std::max(1, std::min(H.B, nsm * engine_ctas_per_sm()));
   QG_CUDA(cudaMemsetAsync(W.d_claim, 0, sizeof(int), st));
+  static const bool want_prof = std::getenv("QG_ENG_PROF") != nullptr;
+  if (want_prof) {
+    if (!H.eng_prof) H.eng_prof = dev_alloc<unsigned long long>(8);
+    QG_CUDA(cudaMemsetAsync(H.eng_prof, 0, 8 * sizeof(unsigned long long), st));
+    a.prof = H.eng_prof;
+  }
   kern<<<grid, nt, smem, st>>>(M, a);
   QG_LAUNCHED();
+  if (want_prof) {
+    unsigned long long h[8];
+    QG_CUDA(cudaMemcpyAsync(h, H.eng_prof, sizeof(h), cudaMemcpyDeviceToHost, st));
+    QG_CUDA(cudaStreamSynchronize(st));
+    const double it = (double)std::max<unsigned long long>(h[5], 1);
+    std::fprintf(stderr, "[qg engine] grid %d x %d thr, smem %zu B, res_cap %d | cycles/iter: A_u %.0f B_u %.0f "
+                 "A_v %.0f B_v %.0f | fin %.0f x2, spmv(warp 1) %.0f x2 | setup/problem %.0f | iters %llu\n", grid, nt,
+                 smem, a.res_cap, h[1] / it, h[2] / it, h[3] / it, h[4] / it, h[6] / it / 2, h[7] / it / 2,
+                 h[0] / (double)H.B, h[5]);
+  }
 }
 
 }  // namespace qg

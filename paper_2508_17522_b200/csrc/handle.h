@@ -84,7 +84,10 @@ struct Handle {
   bool engine = false;          // LSMR solves run problem-resident (engine.cu)
   // engine layout: 16-bit problem-local columns parallel to the SELL entries
   // of P, A', A and 16-bit local rows of the slice lanes (0xffff = padding)
-  uint16_t *c16P = nullptr, *c16AT = nullptr, *c16A = nullptr, *r16x = nullptr, *r16y = nullptr;
+  uint16_t *c16P = nullptr, *c16AT = nullptr, *c16A = nullptr;
+  unsigned char *eng_blob = nullptr;  // per-problem meta blobs (slice table, units, blocks, resident plan)
+  int eng_res_cap = 0;                // resident matrix entries per CTA
+  unsigned long long *eng_prof = nullptr;  // QG_ENG_PROF per-phase cycle counters
   std::vector<Unit> xunits;
   std::vector<int64_t> xunit_ptr;
   Unit *d_xunits = nullptr;
