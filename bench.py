@@ -81,6 +81,10 @@ def init_dist(world, local, backend):
     if world > 1 and not dist.is_initialized():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         if backend == "nccl":
+            # communicator setup lines (ranks, transport, NVLS) in the log: the
+            # evidence that all N ranks formed one NCCL communicator
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -364,7 +368,9 @@ def run_ours(args):
     spmv = "SELL-32" if sx and sy else ("SELL-32/CSR" if sx or sy else "CSR per-unit lanes / CTA-per-row")
     steps_roof = {"kernel": f"k_step<FT> ({spmv} SpMV A,A',P + D Pi x2 epilogue)", "bound": "hbm",
                   "achieved": round(ach, 1), "peak": peaks[0], "peak_source": peaks[1], "unit": "GB/s",
-                  "frac": round(ach / peaks[0], 4), "traffic": _traffic(args.config, ab["FT"], "k_step"),
+                  "frac": round(ach / peaks[0], 4),
+                  **_traffic_fields(_traffic(args.config, ab["FT"], "k_step", args.batch)
+                                    if world == 1 and not b.resident() else None),
                   "alg_bytes_per_launch": ab["FT"], "launch_ms": round(t_ft, 4),
                   "f_step": {"achieved": round(ab["F"] / (t_f / 1e3) / 1e9, 1), "launch_ms": round(t_f, 4),
                              "alg_bytes_per_launch": ab["F"]}}
@@ -380,7 +386,8 @@ def run_ours(args):
         roof = {"kernel": "k_engine (problem-resident LSMR loop: SELL-32 SpMV A,A',P from HBM/L2, vectors in "
                           "shared memory, D Pi epilogues, in-CTA finalize)", "bound": "hbm",
                 "achieved": round(ach_e, 1), "peak": peaks[0], "peak_source": peaks[1], "unit": "GB/s",
-                "frac": round(ach_e / peaks[0], 4), "traffic": _traffic(args.config, alg // 2, "k_engine"),
+                "frac": round(ach_e / peaks[0], 4),
+                **_traffic_fields(_traffic(args.config, alg // 2, "k_engine", args.batch) if world == 1 else None),
                 "alg_bytes_per_launch": alg // 2, "launch_ms": round((lj + lv) / 2, 4),
                 "loop_ms": {"jvp": round(lj, 3), "vjp": round(lv, 3)},
                 "note": "one launch per solve; algorithmic bytes = (B_F + B_F') x iterations of all problems "
@@ -474,12 +481,54 @@ def _dgemm_tflops(dev, n=8192, reps=5):
     return 2 * n ** 3 / (best / 1e3) / 1e12
 
 
-def _traffic(cfg, alg, kernel="k_step"):
-    """dram bytes per launch of the same kernel from the committed ncu capture."""
+def _traffic_fields(t):
+    """roofline keys: "traffic" = DRAM bytes per launch (the contract's
+    number), "traffic_detail" = read / write split and where it came from."""
+    return {"traffic": t["bytes"] if t else None, "traffic_detail": t}
+
+
+def _traffic(cfg, alg, kernel="k_step", batch=None):
+    """DRAM bytes (read + write) per launch of the dominant kernel, captured
+    IN THIS RUN: tools/traffic_probe.py rebuilds this workload and runs the
+    hot path once under `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum` filtered to that kernel (one launch).  Falls back
+    to the committed capture (profiles/traffic.json) when ncu is missing or
+    fails, saying so."""
+    import shutil
+
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
+    if ncu and not os.environ.get("QG_NO_NCU"):
+        filt = ["-k", "regex:^k_engine$"] if kernel == "k_engine" else \
+            ["--kernel-name-base", "mangled", "-k", "regex:k_stepILi1"]
+        cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum", *filt,
+               "-c", "1", "--csv", sys.executable, os.path.join(ROOT, "tools", "traffic_probe.py"),
+               "--config", cfg, "--which", "engine" if kernel == "k_engine" else "ft"]
+        if batch:
+            cmd += ["--batch", str(batch)]
+        try:
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+            vals = {}
+            for line in r.stdout.splitlines():
+                parts = [p.strip('"') for p in line.split('","')]
+                if len(parts) > 3 and parts[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum",
+                                                     "gpu__time_duration.sum"):
+                    unit, v = parts[-2], float(parts[-1].replace(",", ""))
+                    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9,
+                             "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1,
+                             "s": 1}.get(unit, 1)
+                    vals[parts[-3]] = v * scale
+            if "dram__bytes_read.sum" in vals:
+                return {"bytes": int(vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0)),
+                        "read": int(vals["dram__bytes_read.sum"]), "write": int(vals.get("dram__bytes_write.sum", 0)),
+                        "ncu_duration_ms": round(vals.get("gpu__time_duration.sum", 0) * 1e3, 4),
+                        "source": f"ncu in this run ({kernel}, one launch, cold L2)"}
+        except (OSError, subprocess.SubprocessError, ValueError):
+            pass
     path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(path) as f:
-            return json.load(f).get(cfg)
+            v = json.load(f).get(cfg)
+        return None if v is None else {"bytes": v, "source": "profiles/traffic.json (committed capture)"}
     except (OSError, ValueError):
         return None
 

@@ -181,7 +181,7 @@ void ConeTable::prepare(const double *z, double *proj, int dual_mode, bool want_
              want_deriv ? 1 : 0, d_err};
   const size_t smem = psd_smem_prep();
   if (smem > 48 * 1024)
-    QG_CUDA(cudaFuncSetAttribute(k_cone_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    raise_dynamic_smem(reinterpret_cast<const void *>(k_cone_prep), smem);
   k_cone_prep<<<(unsigned)units.size(), kThreads, smem, st>>>(a);
   QG_LAUNCHED();
   if (want_deriv && z != d_zmid)
@@ -220,7 +220,7 @@ void ConeTable::apply(const double *in, double *out, cudaStream_t st) {
   if (units.empty()) return;
   const size_t smem = psd_smem_apply();
   if (smem > 48 * 1024)
-    QG_CUDA(cudaFuncSetAttribute(k_dpi_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    raise_dynamic_smem(reinterpret_cast<const void *>(k_dpi_apply), smem);
   k_dpi_apply<<<(unsigned)units.size(), kThreads, smem, st>>>(view(), d_units, in, out);
   QG_LAUNCHED();
 }

@@ -35,7 +35,10 @@
 // The arithmetic of every row / block / scalar is the graph path's
 // (operator.cu expressions, fin_core through lsmr_dev.cuh); only the CTA
 // summation trees differ (deterministic, fixed order).
+#include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <vector>
 
 #include "dpi_dev.cuh"
 #include "lsmr_dev.cuh"
@@ -96,7 +99,10 @@ struct EngArgs {
   int *next;                   // problem claim counter (zeroed before the launch)
   int B;
   int nmax, mmax;              // vector strides (max n+m+1, max m over the batch)
-  int vec_doubles;             // 3 nmax + mmax rounded up to even
+  // shared-memory byte offsets: u, v, rs (nmax each), dp (mmax), then the
+  // problem's static rows q, P xbar (xmax each), b, z (mmax each), the SOC
+  // parameters nu (double) / code (int) per block (bmax), blob, resident part
+  int o_q, o_px, o_b, o_z, o_nu, o_code, o_blob;
   int res_cap;                 // resident matrix capacity in entries (multiple of 32)
   unsigned long long *prof;    // QG_ENG_PROF=1: SM cycles [setup, A_u, B_u, A_v, B_v, iters, fin, spmv(warp 1)]
 };
@@ -159,7 +165,7 @@ struct EngView {
   const EngArgs &a;
   __device__ __forceinline__ unsigned char *blob() const {
     extern __shared__ __align__(16) double sm[];
-    return reinterpret_cast<unsigned char *>(sm + a.vec_doubles);
+    return reinterpret_cast<unsigned char *>(sm) + a.o_blob;
   }
   __device__ __forceinline__ const EngHead *hd() const { return reinterpret_cast<const EngHead *>(blob()); }
   __device__ __forceinline__ const SliceMeta *sl() const {
@@ -351,6 +357,12 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
                                              const Embed &E, const double *in, double *out, double *rs,
                                              double *dp, double s_in, double c_out, bool upd, const Lsmr &L,
                                              double *red) {
+  extern __shared__ __align__(16) double sm[];
+  const unsigned char *smb = reinterpret_cast<const unsigned char *>(sm);
+  const double *sq = reinterpret_cast<const double *>(smb + a.o_q), *spx = reinterpret_cast<const double *>(smb + a.o_px);
+  const double *bY = reinterpret_cast<const double *>(smb + a.o_b), *zY = reinterpret_cast<const double *>(smb + a.o_z);
+  const double *snu = reinterpret_cast<const double *>(smb + a.o_nu);
+  const int *scode = reinterpret_cast<const int *>(smb + a.o_code);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nt = (int)blockDim.x, nw = nt >> 5;
   const int n = g.n, m = g.m;
@@ -374,8 +386,7 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
     }
   }
   for (int i = tid; i < n; i += nt) {
-    const int64_t r = g.xo + i;
-    const double w = in[i], qr = M.q[r], px = M.Pxbar[r];
+    const double w = in[i], qr = sq[i], px = spx[i];
     double res;
     if (KIND == STEP_F) {
       const double o1 = rs[i] + wN * qr;
@@ -392,7 +403,6 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
   }
   double *outY = out + n;
   const double *inY = in + n;
-  const double *bY = M.b + g.yo, *zY = M.dpi.zmid + g.yo;
   if (KIND == STEP_F) {
     for (int j = tid; j < m; j += nt) {
       const double br = bY[j];
@@ -419,14 +429,17 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
     const int nyu = V.hd()->nyu;
     for (int ui = 0; ui < nyu; ++ui) {
       const EUnit u = V.units()[ui];
+      // rows / blocks go to threads by their problem-local index (not by unit
+      // offsets), so every partial sum -- and the LSMR iterates -- are the same
+      // whatever batch (and hence unit cut) the problem is prepared in
       if (u.cls == CLS_ELEM) {
-        for (int j = u.row0 + tid; j < u.row1; j += nt) {
+        for (int j = u.row0 + (tid - u.row0 % nt + nt) % nt; j < u.row1; j += nt) {
           const double wgt = elem_weight(u.kind, dv.dual, zY[j]);
           const double o = fin_row(j, wgt * tval(j));
           dp[j] = wgt * o;
         }
       } else if (u.cls == CLS_TRI) {
-        for (int k = u.blk0 + tid; k < u.blk1; k += nt) {
+        for (int k = u.blk0 + (tid - u.blk0 % nt + nt) % nt; k < u.blk1; k += nt) {
           const EBlk b = V.blks()[k];
           const int j = b.j0;
           double D[9];
@@ -446,13 +459,14 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
         // G lanes per SOC block (dims <= 32), one lane per row: soc_entry
         // twice (cones.py:740-764) with group shuffle sums
         const int G = u.G, per = 32 / G, lg = lane & (G - 1), src = lane & ~(G - 1);
-        for (int base = u.blk0 + warp * per; base < u.blk1; base += nw * per) {
+        for (int base = (u.blk0 / (nw * per)) * (nw * per) + warp * per; base < u.blk1; base += nw * per) {
           const int k = base + lane / G;
-          const bool kok = k < u.blk1;
+          const bool kok = k >= u.blk0 && k < u.blk1;
           const EBlk b = V.blks()[kok ? k : u.blk0];
+          const int kb = kok ? k : u.blk0;
           const int dim = kok ? b.dim : 0, j0 = b.j0;
-          const int code = dv.soc_code[b.param];
-          const double nu = dv.soc_nu[b.param];
+          const int code = scode[kb];
+          const double nu = snu[kb];
           const bool ok = lg < dim;
           const double zi = ok ? zY[j0 + lg] : 0.0;
           const double ti = ok ? tval(j0 + lg) : 0.0;
@@ -465,11 +479,11 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
         }
       } else {
         // large SOC blocks: a warp per block (soc_apply_warp), t in place in rs
-        for (int k = u.blk0 + warp; k < u.blk1; k += nw) {
+        for (int k = u.blk0 + (warp - u.blk0 % nw + nw) % nw; k < u.blk1; k += nw) {
           const EBlk b = V.blks()[k];
           const int dim = b.dim, j0 = b.j0;
-          const int code = dv.soc_code[b.param];
-          const double nu = dv.soc_nu[b.param];
+          const int code = scode[k];
+          const double nu = snu[k];
           double *tb = rs + n + j0;
           for (int i = lane; i < dim; i += 32) tb[i] = tval(j0 + i);
           __syncwarp();
@@ -494,6 +508,11 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
   constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double *su = sm, *sv = sm + a.nmax, *rs = sm + 2 * a.nmax, *dp = sm + 3 * a.nmax;
+  unsigned char *smb = reinterpret_cast<unsigned char *>(sm);
+  double *sq = reinterpret_cast<double *>(smb + a.o_q), *spx = reinterpret_cast<double *>(smb + a.o_px);
+  double *sb = reinterpret_cast<double *>(smb + a.o_b), *sz = reinterpret_cast<double *>(smb + a.o_z);
+  double *snu = reinterpret_cast<double *>(smb + a.o_nu);
+  int *scode = reinterpret_cast<int *>(smb + a.o_code);
   const EngView V{M, a};
   unsigned char *blob = V.blob();  // 16-byte aligned
   double *resv = V.resv();
@@ -561,6 +580,24 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
     }
     if (a.dp0)
       for (int j = tid; j < m; j += NT) dp[j] = a.dp0[g.yo + j];
+    // the problem's static rows and SOC parameters (read every iteration by
+    // the row epilogues: kept on chip, no global round trip in phase B)
+    for (int i = tid; i < n; i += NT) {
+      sq[i] = M.q[g.xo + i];
+      spx[i] = M.Pxbar[g.xo + i];
+    }
+    for (int j = tid; j < m; j += NT) {
+      sb[j] = M.b[g.yo + j];
+      sz[j] = M.dpi.zmid[g.yo + j];
+    }
+    {
+      const EBlk *gb = reinterpret_cast<const EBlk *>(gblob + a.bl.o_blks);
+      for (int k = tid; k < gh->nblk; k += NT) {
+        const int prm = gb[k].param;
+        snu[k] = M.dpi.soc_nu[prm];
+        scode[k] = M.dpi.soc_code[prm];
+      }
+    }
     if (tid == 0) {
       su[nm] = a.u[g.T];
       sv[nm] = a.v[g.T];
@@ -683,7 +720,8 @@ __global__ void k_engine_meta(Mats M, BlobLayout bl, int res_cap, unsigned char 
   const int kb0 = yu1 > yu0 ? M.yu[yu0].blk0 : 0, kb1 = yu1 > yu0 ? M.yu[yu1 - 1].blk1 : 0;
   const int nxs = xs1 - xs0, nys = ys1 - ys0;
   const int64_t xo = M.xoff[p], yo = M.yoff[p];
-  const int64_t g0[3] = {M.sP.off[xs0], M.sAT.off[xs0], M.sA.off[ys0]};
+  // (a side without slices may have no SELL arrays at all)
+  const int64_t g0[3] = {nxs ? M.sP.off[xs0] : 0, nxs ? M.sAT.off[xs0] : 0, nys ? M.sA.off[ys0] : 0};
   for (int q = threadIdx.x; q < nxs + nys; q += blockDim.x) {
     SliceMeta s{};
     if (q < nxs) {
@@ -732,7 +770,7 @@ __global__ void k_engine_meta(Mats M, BlobLayout bl, int res_cap, unsigned char 
     for (int r : {0, 1, 2}) {  // P, then A' (wide X rows), then A: the streamed rest are narrow Y slices
       int s = sr0[r];
       while (s < sr1[r] && mats[r]->off[s + 1] - g0[r] <= room) ++s;
-      const int ent = (int)(mats[r]->off[s] - g0[r]);
+      const int ent = s > sr0[r] ? (int)(mats[r]->off[s] - g0[r]) : 0;
       h.res[r] = s - sr0[r];
       h.soff[r] = soff;
       h.ent[r] = ent;
@@ -756,17 +794,31 @@ static void engine_dims(const Handle &H, int &nmax, int &mmax) {
 constexpr size_t kEngSmemMax = 227 * 1024 - sizeof(EngShared) - 256;              // one CTA per SM
 constexpr size_t kEngSmemMax2 = 228 * 1024 / 2 - 1024 - sizeof(EngShared) - 256;  // two CTAs per SM
 
-static size_t engine_vec_bytes(const Handle &H) {
-  int nmax, mmax;
+static BlobLayout engine_blob_layout(const Handle &H);
+
+// Shared-memory byte offsets (EngArgs::o_*) of a batch; returns the bytes
+// before the blob.
+static size_t engine_offsets(const Handle &H, int bmax, EngArgs *a) {
+  int nmax, mmax, xmax = 0;
   engine_dims(H, nmax, mmax);
-  return sizeof(double) * (size_t)((3 * nmax + mmax + 1) & ~1);
+  for (int p = 0; p < H.B; ++p) xmax = std::max<int>(xmax, (int)H.n[p]);
+  size_t o = sizeof(double) * (size_t)(3 * nmax + mmax);
+  const size_t oq = o; o += sizeof(double) * xmax;
+  const size_t opx = o; o += sizeof(double) * xmax;
+  const size_t ob = o; o += sizeof(double) * mmax;
+  const size_t oz = o; o += sizeof(double) * mmax;
+  const size_t onu = o; o += sizeof(double) * bmax;
+  const size_t ocode = o; o += sizeof(int) * bmax;
+  o = al16(o);
+  if (a) {
+    a->nmax = nmax;
+    a->mmax = mmax;
+    a->o_q = (int)oq; a->o_px = (int)opx; a->o_b = (int)ob; a->o_z = (int)oz;
+    a->o_nu = (int)onu; a->o_code = (int)ocode; a->o_blob = (int)o;
+  }
+  return o;
 }
 
-// CTA shape (QG_ENG_CFG, A/B): 1 (default) = 512 threads with 128
-// registers, one CTA per SM (c5a loop 85.6 ms per solve, c1 1.3 ms per 148
-// problems); 0 = 1024 threads at 64 registers (spills in the finalize: 89 /
-// 2.0 ms); 2 = 512 threads, two CTAs (problems) per SM with a third of the
-// resident matrix each (96 ms).
 static int engine_cfg() {
   static const char *env = std::getenv("QG_ENG_CFG");
   static const int c = env ? std::max(0, std::min(2, std::atoi(env))) : 1;
@@ -792,7 +844,7 @@ static BlobLayout engine_blob_layout(const Handle &H) {
 
 static int engine_res_cap(const Handle &H, size_t blob_stride) {
   const size_t cap = engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax;
-  const size_t used = engine_vec_bytes(H) + blob_stride;
+  const size_t used = engine_offsets(H, engine_blob_layout(H).bmax, nullptr) + blob_stride;
   int rc = used < cap ? (int)(((cap - used) / 10) & ~size_t(31)) : 0;
   if (const char *e = std::getenv("QG_ENG_RESIDENT")) rc = std::min(rc, std::atoi(e) & ~31);  // A/B
   return rc;
@@ -804,7 +856,9 @@ bool engine_candidate(const Handle &H) {
   if (env && std::atoi(env) == 0) return false;
   for (int p = 0; p < H.B; ++p)
     if (H.n[p] >= 65535 || H.m[p] >= 65535) return false;  // 16-bit local indices
-  if (engine_vec_bytes(H) + 16 * 1024 > (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax)) return false;
+  if (engine_offsets(H, engine_blob_layout(H).bmax, nullptr) + 16 * 1024 >
+      (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax))
+    return false;
   if (env && std::atoi(env) != 0) return true;
   // resident solves win when the batch fills the GPU with problems, or the
   // single problems are small enough that launch latency dominates
@@ -818,7 +872,7 @@ bool engine_units_ok(const Handle &H) {
     for (const Unit &u : *us)
       if (u.mode != MODE_SELL) return false;
   const BlobLayout bl = engine_blob_layout(H);
-  return engine_vec_bytes(H) + bl.stride <= (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax);
+  return engine_offsets(H, bl.bmax, nullptr) + bl.stride <= (engine_ctas_per_sm() == 2 ? kEngSmemMax2 : kEngSmemMax);
 }
 
 static void slice_probs(const std::vector<Unit> &units, int64_t nslices, std::vector<int32_t> &out) {
@@ -862,6 +916,22 @@ void build_engine_layout(Handle &H, cudaStream_t st) {
   dev_free(d_spy);
 }
 
+template <class K>
+static void set_max_dynamic_smem(K kern) {
+  static std::mutex mu;
+  static std::vector<const void *> done;
+  std::lock_guard<std::mutex> lock(mu);
+  const void *key = reinterpret_cast<const void *>(kern);
+  if (std::find(done.begin(), done.end(), key) != done.end()) return;
+  int dev = 0, optin = 0;
+  QG_CUDA(cudaGetDevice(&dev));
+  QG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  cudaFuncAttributes fa{};
+  QG_CUDA(cudaFuncGetAttributes(&fa, kern));
+  QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+  done.push_back(key);
+}
+
 void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st) {
   Workspace &W = H.ws;
   EngArgs a{};
@@ -873,16 +943,18 @@ void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st) {
   a.bl = engine_blob_layout(H);
   a.next = W.d_claim;
   a.B = H.B;
-  engine_dims(H, a.nmax, a.mmax);
-  a.vec_doubles = (3 * a.nmax + a.mmax + 1) & ~1;
+  engine_offsets(H, a.bl.bmax, &a);
   a.res_cap = H.eng_res_cap;
   const int nt = engine_threads();
-  const size_t smem = sizeof(double) * (size_t)a.vec_doubles + a.bl.stride + (size_t)a.res_cap * 10;
+  const size_t smem = (size_t)a.o_blob + a.bl.stride + (size_t)a.res_cap * 10;
   const int cfg = engine_cfg();
   auto kern = cfg == 2 ? (jvp ? k_engine<STEP_F, STEP_FT, 512, 2> : k_engine<STEP_FT, STEP_F, 512, 2>)
               : cfg == 1 ? (jvp ? k_engine<STEP_F, STEP_FT, 512, 1> : k_engine<STEP_FT, STEP_F, 512, 1>)
                          : (jvp ? k_engine<STEP_F, STEP_FT, 1024, 1> : k_engine<STEP_FT, STEP_F, 1024, 1>);
-  QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  // the attribute is per function and process-wide: raise it once to the
+  // opt-in maximum (per-handle sizes set from concurrent host threads would
+  // race each other's launches)
+  set_max_dynamic_smem(kern);
   int dev = 0, nsm = 0;
   QG_CUDA(cudaGetDevice(&dev));
   QG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

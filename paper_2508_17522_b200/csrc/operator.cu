@@ -11,6 +11,9 @@
 //   k_fin       stopping rules                                     (lsmr.py:173-182)
 // The LSMR vectors are kept unnormalised ("raw") with per-problem scale
 // factors, so no kernel has to wait for a norm before writing its output.
+#include <map>
+#include <mutex>
+
 #include "dpi_dev.cuh"
 #include "lsmr_dev.cuh"
 #include "ops_dev.cuh"
@@ -594,6 +597,20 @@ Mats make_mats(const Handle &H) {
   return M;
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per function:
+// only ever raised (handles on concurrent host threads must not lower it
+// under each other's launches).
+void raise_dynamic_smem(const void *kern, size_t bytes) {
+  static std::mutex mu;
+  static std::map<const void *, size_t> raised;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t &r = raised[kern];
+  if (bytes > r) {
+    QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    r = bytes;
+  }
+}
+
 static size_t step_smem(const Handle &H) { return H.cones.max_psd_order ? H.cones.psd_smem_apply() : 0; }
 
 // Launch with programmatic stream serialization (see pdl_wait / pdl_trigger
@@ -663,8 +680,7 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
   const bool sell = H.nslice_x + H.nslice_y > 0;
   const int minb = env_minb ? (std::atoi(env_minb) >= 12 ? 12 : 8) : (sell && kind == STEP_F ? 8 : 12);
   auto go = [&](auto kern, size_t sm_bytes) {
-    if (sm_bytes > 48 * 1024)
-      QG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_bytes));
+    if (sm_bytes > 48 * 1024) raise_dynamic_smem(reinterpret_cast<const void *>(kern), sm_bytes);
     launch_pdl(kern, dim3(grid), dim3(threads), sm_bytes, st, M, a);
   };
   // the CTA-per-row path and the rarely used features run as their own

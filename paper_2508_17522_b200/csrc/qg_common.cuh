@@ -31,6 +31,9 @@ void set_error(int code, const std::string &msg);
 void trace_point(const char *what, cudaStream_t st);  // QG_TRACE diagnostics (api.cu)
 int fail(int code, const std::string &msg);
 void count_launch(int n = 1);
+// cudaFuncAttributeMaxDynamicSharedMemorySize, raised monotonically and
+// thread-safely per kernel (operator.cu)
+void raise_dynamic_smem(const void *kern, size_t bytes);
 
 #define QG_CUDA(expr)                                                              \
   do {                                                                             \

@@ -80,15 +80,24 @@ def test_fixed_cap_matches_reference(name):
     assert _vjp_gap(g, d, "k3") <= 1e-6
 
 
+# The reference's OWN iteration count at tol 1e-14 under 1e-16 operator
+# noise (16 draws, oracle): golden_nonneg jvp 77..80 / vjp 74..82 around 78 /
+# 78 (the instance the reference flags derivative_unreliable; SURVEY §8(c)
+# excludes it from converged parity) -- its stop iteration moves by up to 4
+# for ANY change of summation order, so its slack is twice that.
+ITER_SLACK = {"golden_nonneg": 8}
+
+
 @pytest.mark.parametrize("name", [f"golden_{k}" for k in KINDS] + RECIPES)
 def test_matched_tolerance_matches_reference(name):
     d = load(f"{name}.npz")
     theta, sol, pert, delta = product_instance(d)
+    slack = lambda its: max(3, int(0.05 * its), ITER_SLACK.get(name, 0))
     dl, dg = qg.jvp(theta, sol, pert, atol=1e-14, btol=1e-14)
-    assert abs(dg.iterations - int(d["t14_jvp_its"])) <= max(3, int(0.05 * d["t14_jvp_its"]))
+    assert abs(dg.iterations - int(d["t14_jvp_its"])) <= slack(int(d["t14_jvp_its"]))
     assert _jvp_gap(dl, d, "t14") <= 1e-6
     g, vg = qg.vjp(theta, sol, delta, atol=1e-14, btol=1e-14)
-    assert abs(vg.iterations - int(d["t14_vjp_its"])) <= max(3, int(0.05 * d["t14_vjp_its"]))
+    assert abs(vg.iterations - int(d["t14_vjp_its"])) <= slack(int(d["t14_vjp_its"]))
     assert _vjp_gap(g, d, "t14") <= 1e-6
 
 
@@ -148,9 +157,16 @@ def test_precheck_rejects_bad_solution():
     assert not exc.value.kkt.ok
 
 
-def test_batch_equals_singles():
-    items = [product_instance(load(f"golden_{k}.npz")) for k in KINDS]
+@pytest.mark.parametrize("engine", ["0", "1"])
+def test_batch_equals_singles(monkeypatch, engine):
+    """A problem's iterates do not depend on the batch it is prepared in --
+    within one loop mode (QG_ENGINE=0: the graph loop; 1: the resident
+    engine, which takes no PSD blocks)."""
+    monkeypatch.setenv("QG_ENGINE", engine)
+    kinds = [k for k in KINDS if engine == "0" or k != "psd"]
+    items = [product_instance(load(f"golden_{k}.npz")) for k in kinds]
     batch = qg.QCPBatch([t for t, _, _, _ in items], [s for _, s, _, _ in items])
+    assert batch.resident() == (engine == "1")
     outs = batch.jvp_all([p for _, _, p, _ in items], atol=1e-14, btol=1e-14)
     for (theta, sol, pert, _), (dl, dg) in zip(items, outs):
         one, og = qg.QCP(theta, sol).jvp(pert, atol=1e-14, btol=1e-14)

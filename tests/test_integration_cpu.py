@@ -66,7 +66,7 @@ def test_golden_relaxation_is_per_kind_and_measured():
     for kind in cp.NOISE:
         for op in ("jvp", "vjp"):
             want = helpers.load_golden(f"{kind}_{op}.json")
-            tol, slack = cp.kind_tolerance(want)
+            tol, slack, _ = cp.kind_tolerance(want)
             assert tol >= 1e-6 and slack >= 3
             assert tol == max(1e-6, 10 * cp.NOISE[kind][f"{op}_gap"])
             assert cp.relaxed_golden_result_gap(copy.deepcopy(want), want) == 0.0
@@ -75,4 +75,6 @@ def test_golden_relaxation_is_per_kind_and_measured():
             got[key] = [v + 2.0 * tol * (1.0 + max(abs(x) for x in want[key])) for v in want[key]]
             assert cp.relaxed_golden_result_gap(got, want) > cp.SUITE_TOL
     assert cp.kind_tolerance(helpers.load_golden("soc_jvp.json"))[0] == 1e-6
+    assert cp.kind_tolerance(helpers.load_golden("soc_jvp.json"))[2] is None       # flags exact
     assert cp.kind_tolerance(helpers.load_golden("nonneg_jvp.json"))[0] > 1e-3
+    assert cp.kind_tolerance(helpers.load_golden("zero_vjp.json"))[2] == {(True, False), (True, True)}

@@ -39,6 +39,7 @@ def main(draws=16):
         th, sol, pert, de = instance(d)
         worst_j = worst_v = 0.0
         its_j, its_v = [], []
+        flags_j, flags_v = set(), set()
         for seed in range(draws):
             rng = np.random.default_rng(seed)
 
@@ -49,8 +50,10 @@ def main(draws=16):
 
             Q.make_F = noisy_F
             try:
-                dl, _, dj = Q.jvp(th, sol, pert)
-                gv, _, dv = Q.vjp(th, sol, de)
+                dl, diag_j, dj = Q.jvp(th, sol, pert)
+                gv, diag_v, dv = Q.vjp(th, sol, de)
+                flags_j.add((bool(diag_j.converged), bool(diag_j.derivative_unreliable)))
+                flags_v.add((bool(diag_v.converged), bool(diag_v.derivative_unreliable)))
             finally:
                 Q.make_F = make_F
             worst_j = max(worst_j, sgap(dl.dx, d["jvp_dx"]), sgap(dl.dy, d["jvp_dy"]), sgap(dl.ds, d["jvp_ds"]))
@@ -60,6 +63,8 @@ def main(draws=16):
             its_v.append(dv.itn)
         out[kind] = {"jvp_gap": worst_j, "vjp_gap": worst_v, "jvp_its": [min(its_j), max(its_j)],
                      "vjp_its": [min(its_v), max(its_v)], "golden_its": [int(d["jvp_its"]), int(d["vjp_its"])],
+                     # (converged, derivative_unreliable) pairs the reference itself produced
+                     "jvp_flags": sorted([list(f) for f in flags_j]), "vjp_flags": sorted([list(f) for f in flags_v]),
                      "draws": draws}
     print(json.dumps(out, indent=1))
 
