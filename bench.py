@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=None, help="problems in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=4, help="batch configs: chunks of the host-buffer pipeline")
     return ap.parse_args()
 
 
@@ -335,11 +336,19 @@ def run_ours(args):
                 for k in ("dP", "dA", "dq", "db", "dx", "dy", "ds")}
         outs = {}
 
-        # whole-batch host path; pipeline.evaluate_host (chunked, copies on a
-        # second stream) measured slower on c5a: 324 / 353 ms at 1 / 4 chunks vs
-        # 307 ms -- the library's small preparation copies queue behind the
-        # next chunk's upload in the copy engine
+        # host buffers in, host results out: the batch in `e2e_chunks` chunks
+        # through pipeline.evaluate_host (chunk k+1's upload and chunk k-1's
+        # download overlap chunk k's kernels) or, at 1 chunk / row shards, the
+        # whole-batch from_host + jvp_host + vjp_host path
+        from paper_2508_17522_b200.pipeline import evaluate_host
+
+        chunks = args.e2e_chunks if (args.config in BATCH and comm is None) else 1
+        pout = {}
+
         def step_host():
+            if chunks > 1:
+                pout["o"] = evaluate_host(*sizes, pin, pdir, chunks=chunks, out=pout.get("o", (None,))[0], **kw)
+                return
             outs.clear()  # release last step's pinned result buffers back to torch's host cache
             b = QCPBatch.from_host(*sizes, pin, comm=comm)
             outs["j"] = b.jvp_host(pdir["dP"], pdir["dA"], pdir["dq"], pdir["db"], **kw)
@@ -355,7 +364,8 @@ def run_ours(args):
         d2h = 8 * (sum(bt.n) * 2 + sum(bt.m) * 3 + bt.P_vals.size + bt.A_vals.size)
         e2e = {"value": units_total / (ems / 1e3), "unit": "evals/s", "h2d_bytes_per_step": int(h2d * world),
                "d2h_bytes_per_step": int(d2h * world), "ms_per_step": ems,
-               "api": "QCPBatch.from_host + jvp_host + vjp_host (pinned host buffers)"}
+               "api": (f"pipeline.evaluate_host, {chunks} chunks (pinned host buffers; copies overlap kernels)"
+                       if chunks > 1 else "QCPBatch.from_host + jvp_host + vjp_host (pinned host buffers)")}
 
     # roofline of the fused kernels (CUDA events inside the library, same stream)
     b = step_device()

@@ -73,7 +73,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(d_claim); dev_free(rk1);
+  dev_free(st); dev_free(d_nactive); dev_free(d_claim); dev_free(d_loop); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -113,7 +113,7 @@ Handle::~Handle() {
   sP.release(); sAT.release(); sA.release();
   dev_free(x_rowof); dev_free(y_rowof);
   dev_free(c16P); dev_free(c16AT); dev_free(c16A); dev_free(eng_blob); dev_free(eng_prof);
-  dev_free(d_xunits); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
+  dev_free(d_xunits); dev_free(d_ft_order); dev_free(d_xoff); dev_free(d_yoff); dev_free(d_xunit_ptr); dev_free(d_yunit_ptr);
   dev_free(q); dev_free(b); dev_free(xbar); dev_free(ybar); dev_free(sbar); dev_free(Pxbar); dev_free(emb);
   dev_free(xred); dev_free(psum); dev_free(d_iota);
   ws.release();
@@ -252,6 +252,19 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     build_engine_layout(H, st);
     trace("engine layout");
   }
+  if (H.cones.max_psd_order > 0) {
+    // F' launch order: PSD units first (k_step), then every other unit
+    std::vector<int32_t> order;
+    order.reserve(H.nxu() + H.nyu());
+    for (int u = 0; u < H.nyu(); ++u)
+      if (H.cones.units[u].cls == CLS_PSD) order.push_back(H.nxu() + u);
+    for (int u = 0; u < H.nxu(); ++u) order.push_back(u);
+    for (int u = 0; u < H.nyu(); ++u)
+      if (H.cones.units[u].cls != CLS_PSD) order.push_back(H.nxu() + u);
+    H.d_ft_order = dev_alloc<int32_t>(order.size());
+    QG_CUDA(cudaMemcpyAsync(H.d_ft_order, order.data(), sizeof(int32_t) * order.size(), cudaMemcpyHostToDevice, st));
+    QG_CUDA(cudaStreamSynchronize(st));  // host vector
+  }
 
   // problem vectors
   H.q = dev_alloc<double>(H.NX);
@@ -277,6 +290,7 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.st = dev_alloc<Lsmr>(B);
   W.d_nactive = dev_alloc<int>(1);
   W.d_claim = dev_alloc<int>(1);
+  W.d_loop = dev_alloc<long long>(2);
   W.h_nactive = nullptr;
   if (H.comm) {
     H.xred = dev_alloc<double>(H.NX);
@@ -382,7 +396,48 @@ static cudaGraph_t capture_graph(Handle &H, const Mats &M, bool jvp, int iters) 
   return graph;
 }
 
-// Launch `iters` LSMR iterations of handle H as one graph on `st`.
+// The whole LSMR loop as ONE graph: a conditional WHILE node whose body is
+// `chunk` iterations plus k_loop_cond, which re-arms the node while a
+// problem is active and the cap (W.d_loop[1]) is not reached.  No host
+// round trip between chunks (the host-polled loop counted active problems
+// and synchronised the stream before every chunk).
+constexpr int kWhileChunk = 4;
+
+static cudaGraph_t capture_while_graph(Handle &H, const Mats &M, bool jvp, int chunk) {
+  cudaGraph_t g;
+  QG_CUDA(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  QG_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams p{};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = cudaGraphCondTypeWhile;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  QG_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &p));
+  cudaGraph_t body = p.conditional.phGraph_out[0];
+  cudaStream_t cs;
+  QG_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  QG_CUDA(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  const long long before = g_launches.load();
+  cudaGraph_t out;
+  try {
+    capture_iters(H, M, jvp, chunk, cs);
+    launch_loop_cond(H, h, chunk, cs);
+  } catch (...) {
+    cudaStreamEndCapture(cs, &out);
+    cudaStreamDestroy(cs);
+    cudaGraphDestroy(g);
+    throw;
+  }
+  g_launches = before;  // counted from the iterations actually run (lsmr_finish)
+  QG_CUDA(cudaStreamEndCapture(cs, &out));
+  cudaStreamDestroy(cs);
+  return g;
+}
+
+// Launch `iters` LSMR iterations of handle H as one graph on `st`
+// (iters = -kWhileChunk: the device-terminated WHILE graph).
 static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
   if (H.comm && !H.comm->capturable()) {  // host-synchronised exchange: plain launches
     capture_iters(H, M, jvp, iters, st);
@@ -395,7 +450,9 @@ static void launch_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStre
   if (git == g_graphs.end()) git = g_graphs.emplace(&H, new GraphCache()).first;
   GraphCache *gc = git->second;
   auto cit = gc->graph.find(key);
-  if (cit == gc->graph.end()) cit = gc->graph.emplace(key, capture_graph(H, M, jvp, iters)).first;
+  if (cit == gc->graph.end())
+    cit = gc->graph.emplace(key, iters < 0 ? capture_while_graph(H, M, jvp, -iters) : capture_graph(H, M, jvp, iters))
+              .first;
   SharedExec &se = g_exec[ExecKey{st, key.first, key.second}];
   if (se.exec == nullptr) {
     QG_CUDA(cudaGraphInstantiate(&se.exec, cit->second, 0));
@@ -430,6 +487,13 @@ static int kernels_per_iter(const Handle &H) {
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
   Workspace &W = H.ws;
+  const char *env = std::getenv("QG_HOST_LOOP");  // A/B: the host-polled chunk loop
+  if ((!H.comm || H.comm->capturable()) && !(env && std::atoi(env) != 0)) {
+    // W.d_loop = [0, cap] was armed by k_init_state
+    if (cap > 0) launch_iters(H, M, jvp, -kWhileChunk, st);
+    H.while_pending = true;
+    return;
+  }
   long long done = 0;
   while (true) {
     launch_count_active(H, st);
@@ -448,20 +512,15 @@ static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cud
 }
 
 static void lsmr_begin(Handle &H, const qg_lsmr_opts &o, cudaStream_t st, long long &cap) {
-  std::vector<long long> mi(H.B);
   cap = 0;
   for (int p = 0; p < H.B; ++p) {
     const long long N = H.n[p] + H.m[p] + 1;
     // lsmr.py:69-70: None -> 10 * (in + out); the ABI encodes None as 0 and an
-    // explicit cap of zero as a negative value
-    mi[p] = (o.max_iter > 0) ? o.max_iter : (o.max_iter < 0 ? 0 : 20 * N);
-    cap = std::max(cap, mi[p]);
+    // explicit cap of zero as a negative value (k_init_state applies the same
+    // rule per problem on the device)
+    cap = std::max(cap, (o.max_iter > 0) ? (long long)o.max_iter : (o.max_iter < 0 ? 0LL : 20 * N));
   }
-  long long *d_mi = dev_alloc<long long>(H.B);
-  QG_CUDA(cudaMemcpyAsync(d_mi, mi.data(), sizeof(long long) * H.B, cudaMemcpyHostToDevice, st));
-  launch_init_state(H, o.atol, o.btol, d_mi, st);
-  QG_CUDA(cudaStreamSynchronize(st));
-  dev_free(d_mi);
+  launch_init_state(H, o.atol, o.btol, o.max_iter, cap, st);
   Workspace &W = H.ws;
   QG_CUDA(cudaMemsetAsync(W.x, 0, sizeof(double) * H.NE, st));
   QG_CUDA(cudaMemsetAsync(W.h, 0, sizeof(double) * H.NE, st));
@@ -472,6 +531,13 @@ static void lsmr_finish(Handle &H, qg_diag *diag, cudaStream_t st) {
   std::vector<Lsmr> L(H.B);
   QG_CUDA(cudaMemcpyAsync(L.data(), H.ws.st, sizeof(Lsmr) * H.B, cudaMemcpyDeviceToHost, st));
   QG_CUDA(cudaStreamSynchronize(st));
+  if (H.while_pending) {
+    long long run[2] = {0, 0};
+    QG_CUDA(cudaMemcpyAsync(run, H.ws.d_loop, sizeof(run), cudaMemcpyDeviceToHost, st));
+    QG_CUDA(cudaStreamSynchronize(st));
+    count_launch((run[0] / kWhileChunk) * (kWhileChunk * kernels_per_iter(H) + 1));
+    H.while_pending = false;
+  }
   if (H.loop_pending) {
     float ms = 0.0f;
     if (cudaEventElapsedTime(&ms, H.ev_loop[0], H.ev_loop[1]) == cudaSuccess) H.loop_ms[H.loop_pending - 1] = ms;

@@ -63,6 +63,7 @@ struct Workspace {
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
   int *d_claim = nullptr;    // problem claim counter of the resident engine
+  long long *d_loop = nullptr;  // device-terminated graph loop: [iterations run, cap]
   int *h_nactive = nullptr;  // pinned
   void release();
 };
@@ -93,6 +94,7 @@ struct Handle {
   Unit *d_xunits = nullptr;
   int64_t *d_xoff = nullptr, *d_yoff = nullptr;
   int64_t *d_xunit_ptr = nullptr, *d_yunit_ptr = nullptr;
+  int32_t *d_ft_order = nullptr;  // F' CTA -> unit order, PSD units first (null: natural order)
   double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;
   double *Pxbar = nullptr;
   Embed *emb = nullptr;
@@ -115,6 +117,7 @@ struct Handle {
   cudaEvent_t ev_loop[2] = {nullptr, nullptr};
   double loop_ms[2] = {0.0, 0.0};
   int loop_pending = 0;  // 1: jvp, 2: vjp events recorded, not yet read
+  bool while_pending = false;  // a device-terminated loop ran: count its launches at finish
   void loop_events();
 
   int nxu() const { return (int)xunits.size(); }

@@ -385,9 +385,14 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
 }
 
+// F' launches of batches with PSD blocks take their units in M.ft_order:
+// the PSD units (two D Pi applications of 4 dense products each: the
+// longest CTAs) first, so they start in the first wave instead of forming
+// the launch's tail.
 template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
-  step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, (int)blockIdx.x);
+  const int ui = (KIND == STEP_FT && M.ft_order) ? M.ft_order[blockIdx.x] : (int)blockIdx.x;
+  step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, ui);
 }
 
 // -------------------------------------------------------------- update --
@@ -566,13 +571,50 @@ __global__ void k_count_active(const Lsmr *st, int B, int *out) {
   if (threadIdx.x == 0) *out = cnt;
 }
 
-__global__ void k_init_state(Lsmr *st, int B, double atol, double btol, const long long *max_iter) {
+// Body tail of the device-terminated LSMR loop (a CUDA-graph conditional
+// WHILE node): count the still-active problems, advance the iteration
+// counter by one body (chunk iterations) and let the graph repeat the body
+// only while some problem is active and the cap is not reached -- the
+// control decision of lsmr.py's loop without a host round trip.
+// loop[0] = iterations run, loop[1] = cap.
+__global__ void k_loop_cond(const Lsmr *st, int B, long long *loop, long long chunk, cudaGraphConditionalHandle h) {
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  int c = 0;
+  for (int p = threadIdx.x; p < B; p += blockDim.x) c += st[p].active ? 1 : 0;
+  if (c) atomicAdd(&cnt, c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const long long done = loop[0] + chunk;
+    loop[0] = done;
+    cudaGraphSetConditional(h, (cnt > 0 && done < loop[1]) ? 1u : 0u);
+  }
+}
+
+void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long chunk, cudaStream_t st) {
+  k_loop_cond<<<1, 256, 0, st>>>(H.ws.st, H.B, H.ws.d_loop, chunk, h);
+  QG_LAUNCHED();
+}
+
+// Fresh LSMR state per problem, its iteration cap computed on the device
+// (no host-to-device copy: a chunked host pipeline keeps the copy engine busy
+// with the next chunk's upload): opt > 0 explicit cap, opt < 0 explicit 0,
+// opt == 0 the reference default 20 (n + m + 1) (lsmr.py:69-70 on the
+// embedding).  Thread 0 also arms the device-terminated loop: [0, cap].
+__global__ void k_init_state(Lsmr *st, int B, double atol, double btol, long long opt, const int64_t *xoff,
+                             const int64_t *yoff, long long *loop, long long cap) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p == 0 && loop) {
+    loop[0] = 0;
+    loop[1] = cap;
+  }
   if (p >= B) return;
   Lsmr L{};
   L.atol = atol;
   L.btol = btol;
-  L.max_iter = max_iter[p];
+  const long long N = (xoff[p + 1] - xoff[p]) + (yoff[p + 1] - yoff[p]) + 1;
+  L.max_iter = opt > 0 ? opt : (opt < 0 ? 0 : 20 * N);
   L.s_u = L.s_v = 1.0;
   st[p] = L;
 }
@@ -594,6 +636,7 @@ Mats make_mats(const Handle &H) {
   M.x_rowof = H.x_rowof; M.y_rowof = H.y_rowof;
   M.xoff = H.d_xoff; M.yoff = H.d_yoff;
   M.x_owner = H.x_owner() ? 1 : 0;
+  M.ft_order = H.d_ft_order;
   return M;
 }
 
@@ -744,8 +787,8 @@ void launch_count_active(const Handle &H, cudaStream_t st) {
   QG_LAUNCHED();
 }
 
-void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st) {
-  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, d_max_iter);
+void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st) {
+  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, opt, H.d_xoff, H.d_yoff, H.ws.d_loop, cap);
   QG_LAUNCHED();
 }
 

@@ -62,8 +62,9 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t s
 void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole-problem handle
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
 void launch_count_active(const Handle &H, cudaStream_t st);
-void launch_init_state(const Handle &H, double atol, double btol, const long long *d_max_iter, cudaStream_t st);
+void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st);
 void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st);
+void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long chunk, cudaStream_t st);
 
 // assembly (assembly.cu)
 struct PertDev {

@@ -21,6 +21,7 @@ struct Mats {
   const int32_t *x_rowof, *y_rowof;     // lane -> row per slice (-1 = padding)
   const int64_t *xoff, *yoff;           // [B+1] problem offsets in X / Y
   int x_owner;                          // 0: X rows are replicated and counted by rank 0 only
+  const int32_t *ft_order;              // F' launch order of the units (PSD first), or null
 };
 
 // Row-partitioned mode, X side of an operator step / rhs assembly:

@@ -11,11 +11,12 @@ Problems are independent, so per-problem results equal a whole-batch call up
 to rounding (the work-unit partition, and with it the order of the partial
 sums, depends on the batch size).
 
-Measured on c5a (4096 problems, one B200): 324 / 324 / 353 / 406 ms at 1 / 2
-/ 4 / 8 chunks vs 307 ms for the whole-batch ``from_host`` path -- the
-library's small (pageable) preparation copies queue behind the next chunk's
-upload in the copy engine, so the overlap does not pay yet; bench.py keeps
-the whole-batch path for ``e2e``.
+The next chunk's upload is issued after the current chunk's preparation
+(whose small row-pointer / unit-table copies would otherwise queue behind
+it in the copy engine), and the LSMR setup does no host-to-device copy (the
+caps are computed on the device), so the uploads overlap only kernels.
+Round 1 issued the upload first and measured 324 / 324 / 353 / 406 ms at
+1 / 2 / 4 / 8 chunks vs 307 ms for the whole-batch path.
 """
 
 import numpy as np
@@ -91,11 +92,14 @@ def evaluate_host(n, m, P_nnz, A_nnz, blocks, data, dirs, *, chunks=4, atol=1e-1
     for c in range(len(bounds) - 1):
         lo, hi = bounds[c], bounds[c + 1]
         t, ev = pending
-        if c + 2 < len(bounds):
-            pending = upload(bounds[c + 1], bounds[c + 2])   # next chunk's H2D overlaps this compute
         comp.wait_event(ev)
         b = QCPBatch.from_device(n[lo:hi], m[lo:hi], P_nnz[lo:hi], A_nnz[lo:hi], blocks[lo:hi],
                                  {k: t[k] for k in _DATA})
+        # the next chunk's H2D starts only now, overlapping this chunk's
+        # jvp / vjp kernels: the preparation's own small copies (row
+        # pointers, unit tables) must not queue behind it in the copy engine
+        if c + 2 < len(bounds):
+            pending = upload(bounds[c + 1], bounds[c + 2])
         dx, dy, ds, dj = b.jvp_device(t["dP"], t["dA"], t["dq"], t["db"], **kw)
         gP, gA, gq, gb, dv = b.vjp_device(t["dx"], t["dy"], t["ds"], **kw)
         b.close()

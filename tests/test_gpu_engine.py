@@ -150,3 +150,27 @@ def test_engine_deterministic(monkeypatch):
     r2 = _run(b, dirs, 7)
     for a, c in zip(r1[0] + r1[1], r2[0] + r2[1]):
         assert np.array_equal(a, c)
+
+
+@pytest.mark.parametrize("kw", [dict(atol=0.0, btol=0.0, max_iter=10), dict(atol=1e-12, btol=1e-12),
+                                dict(atol=0.0, btol=0.0, max_iter=3)])
+def test_device_terminated_graph_loop_matches_host_loop(monkeypatch, kw):
+    """The graph loop's conditional WHILE node (k_loop_cond re-arms it while a
+    problem is active and the cap is not reached) runs the same kernels in
+    the same order as the host-polled chunk loop: bit-identical outputs and
+    iteration counts, including caps that are not a multiple of its chunk."""
+    monkeypatch.setenv("QG_ENGINE", "0")
+    bt = synth.generate("c5a", seed=32, batch=3)
+    dirs = synth.directions(bt, seed=33)
+    res = []
+    for host in ("0", "1"):
+        monkeypatch.setenv("QG_HOST_LOOP", host)
+        b = _batch(bt)
+        assert not b.resident()
+        j = b.jvp_device(_dev(dirs.dP), _dev(dirs.dA), _dev(dirs.dq), _dev(dirs.db), **kw)
+        v = b.vjp_device(_dev(dirs.dx), _dev(dirs.dy), _dev(dirs.ds), **kw)
+        res.append(([t.cpu().numpy() for t in j[:3]] + [t.cpu().numpy() for t in v[:4]],
+                    [d.iterations for d in j[3]] + [d.iterations for d in v[4]]))
+    for a, c in zip(res[0][0], res[1][0]):
+        assert np.array_equal(a, c)
+    assert res[0][1] == res[1][1]

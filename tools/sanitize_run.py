@@ -1,8 +1,11 @@
 """Small jvp + vjp workload for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): every golden cone kind (SOC, PSD, exp/pow and
-their duals, zero, nonneg), the c1 shape, a SELL-forced c5a mini-batch and
-a CTA-per-row (MODE_WIDE) problem -- i.e. every step-kernel variant, the
-PSD DMMA epilogue, both finalize kernels, preparation and assembly.
+their duals, zero, nonneg) through BOTH loop modes (the resident engine
+k_engine -- TMA bulk copies, mbarrier, warp-0 finalize overlapping the
+SpMV -- and the graph loop), the c1 shape, a SELL-forced c5a mini-batch
+through both, and a CTA-per-row (MODE_WIDE) problem -- i.e. every
+step-kernel variant, the PSD DMMA epilogue, both finalize kernels, the
+engine, preparation and assembly.
 
     compute-sanitizer --tool racecheck python tools/sanitize_run.py
 """
@@ -39,22 +42,27 @@ def batch_run(bt, dirs, K):
 
 
 def main():
-    for kind in KINDS:
-        theta, sol, pert, delta = product_instance(load(f"golden_{kind}.npz"))
-        q = qg.QCP(theta, sol)
-        q.jvp(pert, max_iter=30)
-        q.vjp(delta, max_iter=30)
-        q.kkt()
-        q.close()
-        print("golden", kind, "ok", flush=True)
+    for engine in ("1", "0"):
+        os.environ["QG_ENGINE"] = engine
+        for kind in KINDS:
+            theta, sol, pert, delta = product_instance(load(f"golden_{kind}.npz"))
+            q = qg.QCP(theta, sol)
+            q.jvp(pert, max_iter=30)
+            q.vjp(delta, max_iter=30)
+            q.kkt()
+            print("golden", kind, "engine" if q.resident() else "graph", "ok", flush=True)
+            q.close()
+    del os.environ["QG_ENGINE"]
     bt = synth.generate("c1", seed=1)
     batch_run(bt, synth.directions(bt, seed=2), 20)
     print("c1 ok", flush=True)
-    os.environ["QG_SELL"] = "1"
     bt = synth.generate("c5a", seed=3, batch=3)
-    batch_run(bt, synth.directions(bt, seed=4), 10)
-    del os.environ["QG_SELL"]
-    print("c5a SELL ok", flush=True)
+    for engine in ("1", "0"):
+        os.environ["QG_ENGINE"] = engine
+        os.environ["QG_SELL"] = "1"
+        batch_run(bt, synth.directions(bt, seed=4), 10)
+        print("c5a SELL", "engine" if engine == "1" else "graph", "ok", flush=True)
+    del os.environ["QG_SELL"], os.environ["QG_ENGINE"]
     # a dense-row problem: MODE_WIDE units (rows of >= 512 entries)
     bt = synth.custom([("zero", 40, 0, 0.0), ("nonneg", 40, 0, 0.0)], n=1200, nnzA=80 * 1100, seed=5)
     batch_run(bt, synth.directions(bt, seed=6), 10)
