@@ -75,17 +75,18 @@ struct EBlk {                      // a cone block: parameter index, local row, 
   uint16_t j0, dim;
 };
 struct BlobLayout {
-  int smax, umax, bmax;
-  size_t o_slices, o_rows, o_units, o_blks, stride;
+  int smax, umax, bmax, mmax;
+  size_t o_slices, o_rows, o_units, o_blks, o_rowblk, stride;
 };
 static __host__ __device__ inline size_t al16(size_t x) { return (x + 15) & ~size_t(15); }
-static __host__ __device__ inline BlobLayout blob_layout(int smax, int umax, int bmax) {
-  BlobLayout L{smax, umax, bmax, 0, 0, 0, 0, 0};
+static __host__ __device__ inline BlobLayout blob_layout(int smax, int umax, int bmax, int mmax) {
+  BlobLayout L{smax, umax, bmax, mmax, 0, 0, 0, 0, 0, 0};
   L.o_slices = al16(sizeof(EngHead));
   L.o_rows = al16(L.o_slices + sizeof(SliceMeta) * (size_t)smax);
   L.o_units = al16(L.o_rows + sizeof(uint16_t) * 32 * (size_t)smax);
   L.o_blks = al16(L.o_units + sizeof(EUnit) * (size_t)umax);
-  L.stride = al16(L.o_blks + sizeof(EBlk) * (size_t)bmax);
+  L.o_rowblk = al16(L.o_blks + sizeof(EBlk) * (size_t)bmax);
+  L.stride = al16(L.o_rowblk + sizeof(uint16_t) * (size_t)mmax);  // Y row -> its cone block (local)
   return L;
 }
 
@@ -102,7 +103,7 @@ struct EngArgs {
   // shared-memory byte offsets: u, v, rs (nmax each), dp (mmax), then the
   // problem's static rows q, P xbar (xmax each), b, z (mmax each), the SOC
   // parameters nu (double) / code (int) per block (bmax), blob, resident part
-  int o_q, o_px, o_b, o_z, o_nu, o_code, o_blob;
+  int o_q, o_px, o_b, o_z, o_nu, o_code, o_scr, o_blob;
   int res_cap;                 // resident matrix capacity in entries (multiple of 32)
   unsigned long long *prof;    // QG_ENG_PROF=1: SM cycles [setup, A_u, B_u, A_v, B_v, iters, fin, spmv(warp 1)]
 };
@@ -112,7 +113,7 @@ struct EngShared {
   double red[kEngMaxWarps * 2 * kSlots];
   double tvh[3];      // T entries of h, hbar, x
   unsigned long long mbar;
-  unsigned long long prof[8];
+  unsigned long long prof[10];
   int p;
 };
 
@@ -176,6 +177,9 @@ struct EngView {
   }
   __device__ __forceinline__ const EUnit *units() const { return reinterpret_cast<const EUnit *>(blob() + a.bl.o_units); }
   __device__ __forceinline__ const EBlk *blks() const { return reinterpret_cast<const EBlk *>(blob() + a.bl.o_blks); }
+  __device__ __forceinline__ const uint16_t *rowblk() const {
+    return reinterpret_cast<const uint16_t *>(blob() + a.bl.o_rowblk);
+  }
   __device__ __forceinline__ double *resv() const { return reinterpret_cast<double *>(blob() + a.bl.stride); }
   __device__ __forceinline__ uint16_t *resc() const { return reinterpret_cast<uint16_t *>(resv() + a.res_cap); }
   __device__ __forceinline__ const double *gval(int r) const {
@@ -206,7 +210,8 @@ __device__ __forceinline__ uint16_t ldc(const uint16_t *p, uint64_t pol) {
 // Each sum runs in storage order.
 template <bool RA, bool RB>
 __device__ __forceinline__ void dot2(const double *va, const uint16_t *ca, int wa, const double *vb,
-                                     const uint16_t *cb, int wb, const double *vec, double &sa, double &sb) {
+                                     const uint16_t *cb, int wb, const double *vec, int vlen, double &sa,
+                                     double &sb) {
   const uint64_t pol = (RA && RB) ? 0 : l2_keep_policy();
   double a = 0.0, b = 0.0;
   const int wm = wa < wb ? wa : wb;
@@ -223,6 +228,7 @@ __device__ __forceinline__ void dot2(const double *va, const uint16_t *ca, int w
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      QG_CHECK(ka[j] < vlen && kb[j] < vlen);
       a += xa[j] * vec[ka[j]];
       b += xb[j] * vec[kb[j]];
     }
@@ -230,6 +236,7 @@ __device__ __forceinline__ void dot2(const double *va, const uint16_t *ca, int w
   for (; k < wm; ++k) {
     const double x1 = ldv<RA>(va + 32 * k, pol), x2 = ldv<RB>(vb + 32 * k, pol);
     const uint16_t k1 = ldc<RA>(ca + 32 * k, pol), k2 = ldc<RB>(cb + 32 * k, pol);
+    QG_CHECK(k1 < vlen && k2 < vlen);
     a += x1 * vec[k1];
     b += x2 * vec[k2];
   }
@@ -255,25 +262,29 @@ __device__ __forceinline__ void dot2(const double *va, const uint16_t *ca, int w
 // widths wa / wb (wb = 0: none); slice a resident iff ra (b resident only if
 // a is: resident slices are a prefix and qa < qb).
 __device__ __forceinline__ void region_dot2(const EngView &V, int r, bool ra, int oa, int wa, bool rb, int ob, int wb,
-                                            int lane, const double *vec, double &sa, double &sb) {
+                                            int lane, const double *vec, int vlen, double &sa, double &sb) {
+  QG_CHECK(!ra || V.hd()->soff[r] + oa + 32 * wa <= V.hd()->soff[r] + V.hd()->ent[r]);
+  QG_CHECK(!(ra && rb && wb > 0) || V.hd()->soff[r] + ob + 32 * wb <= V.hd()->soff[r] + V.hd()->ent[r]);
+  QG_CHECK(V.hd()->soff[r] + V.hd()->ent[r] <= V.a.res_cap);
   const int so = V.hd()->soff[r] + lane;
   const double *rv = V.resv() + so;
   const uint16_t *rc = V.resc() + so;
   const double *gv = V.gval(r) + lane;
   const uint16_t *gc = V.gcol(r) + lane;
   if (ra && (rb || wb == 0))
-    dot2<true, true>(rv + oa, rc + oa, wa, rv + ob, rc + ob, wb, vec, sa, sb);
+    dot2<true, true>(rv + oa, rc + oa, wa, rv + ob, rc + ob, wb, vec, vlen, sa, sb);
   else if (ra)
-    dot2<true, false>(rv + oa, rc + oa, wa, gv + ob, gc + ob, wb, vec, sa, sb);
+    dot2<true, false>(rv + oa, rc + oa, wa, gv + ob, gc + ob, wb, vec, vlen, sa, sb);
   else
-    dot2<false, false>(gv + oa, gc + oa, wa, gv + ob, gc + ob, wb, vec, sa, sb);
+    dot2<false, false>(gv + oa, gc + oa, wa, gv + ob, gc + ob, wb, vec, vlen, sa, sb);
 }
 
 // Phase A: the row sums of one operator application into rs (X rows: P w1
 // +- A' (D Pi) w2 ; Y rows: A w1).  Warp w takes slices w, w + nw, ...,
 // two per round when both are on the same side (their loads overlap).
 template <int KIND>
-__device__ __forceinline__ void eng_spmv(const EngView &V, int n, const double *in, const double *dp, double *rs) {
+__device__ __forceinline__ void eng_spmv(const EngView &V, int n, int m, const double *in, const double *dp,
+                                         double *rs) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   const int nxs = V.hd()->nxs, ntot = nxs + V.hd()->nys;
   const double *x2 = KIND == STEP_F ? dp : in + n;  // A' gathers D Pi w_2 (F) or w_2 (F')
@@ -287,17 +298,18 @@ __device__ __forceinline__ void eng_spmv(const EngView &V, int n, const double *
       if (qa < nxs) {
         double ta, tb;
         region_dot2(V, 0, qa < V.hd()->res[0], ma.off0, ma.w0, !two || qb < V.hd()->res[0], mb.off0,
-                                   two ? mb.w0 : 0, lane, in, sa, sb);
+                                   two ? mb.w0 : 0, lane, in, n, sa, sb);
         region_dot2(V, 1, qa < V.hd()->res[1], ma.off1, ma.w1, !two || qb < V.hd()->res[1], mb.off1,
-                                   two ? mb.w1 : 0, lane, x2, ta, tb);
+                                   two ? mb.w1 : 0, lane, x2, m, ta, tb);
         sa = KIND == STEP_F ? (sa + ta) : (sa - ta);
         sb = KIND == STEP_F ? (sb + tb) : (sb - tb);
       } else {
         region_dot2(V, 2, qa - nxs < V.hd()->res[2], ma.off1, ma.w1, !two || qb - nxs < V.hd()->res[2],
-                                   mb.off1, two ? mb.w1 : 0, lane, in, sa, sb);
+                                   mb.off1, two ? mb.w1 : 0, lane, in, n, sa, sb);
       }
       const int ya = qa < nxs ? 0 : n;
       const uint16_t ra = V.rows()[qa * 32 + lane];
+      QG_CHECK(ra == kPad16 || ra < (qa < nxs ? n : m));
       if (ra != kPad16) rs[ya + ra] = sa;
       if (two) {
         const uint16_t rb = V.rows()[qb * 32 + lane];
@@ -356,8 +368,10 @@ template <int KIND>
 __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, const EngView &V, const Geo &g,
                                              const Embed &E, const double *in, double *out, double *rs,
                                              double *dp, double s_in, double c_out, bool upd, const Lsmr &L,
-                                             double *red) {
+                                             double *red, unsigned long long *prof = nullptr) {
   extern __shared__ __align__(16) double sm[];
+  const bool tp = prof != nullptr && threadIdx.x == 0;  // QG_ENG_PROF: sub-phase cycles of thread 0
+  long long t0c = tp ? clock64() : 0;
   const unsigned char *smb = reinterpret_cast<const unsigned char *>(sm);
   const double *sq = reinterpret_cast<const double *>(smb + a.o_q), *spx = reinterpret_cast<const double *>(smb + a.o_px);
   const double *bY = reinterpret_cast<const double *>(smb + a.o_b), *zY = reinterpret_cast<const double *>(smb + a.o_z);
@@ -427,6 +441,11 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
     };
     const DpiView &dv = M.dpi;
     const int nyu = V.hd()->nyu;
+    if (tp) {
+      const long long t = clock64();
+      prof[8] += (unsigned long long)(t - t0c);  // update + X rows
+      t0c = t;
+    }
     for (int ui = 0; ui < nyu; ++ui) {
       const EUnit u = V.units()[ui];
       // rows / blocks go to threads by their problem-local index (not by unit
@@ -456,26 +475,39 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
           for (int i = 0; i < 3; ++i) dp[j + i] = d3[i];
         }
       } else if (u.G > 0) {
-        // G lanes per SOC block (dims <= 32), one lane per row: soc_entry
-        // twice (cones.py:740-764) with group shuffle sums
-        const int G = u.G, per = 32 / G, lg = lane & (G - 1), src = lane & ~(G - 1);
-        for (int base = (u.blk0 / (nw * per)) * (nw * per) + warp * per; base < u.blk1; base += nw * per) {
-          const int k = base + lane / G;
-          const bool kok = k >= u.blk0 && k < u.blk1;
-          const EBlk b = V.blks()[kok ? k : u.blk0];
-          const int kb = kok ? k : u.blk0;
-          const int dim = kok ? b.dim : 0, j0 = b.j0;
-          const int code = scode[kb];
-          const double nu = snu[kb];
-          const bool ok = lg < dim;
-          const double zi = ok ? zY[j0 + lg] : 0.0;
-          const double ti = ok ? tval(j0 + lg) : 0.0;
-          const double udu = gsum((ok && lg > 0) ? zi * ti : 0.0, G);
-          const double t0 = __shfl_sync(0xffffffffu, zi, src), dt = __shfl_sync(0xffffffffu, ti, src);
-          const double oi = ok ? fin_row(j0 + lg, soc_entry(code, lg, nu, t0, zi, ti, dt, udu)) : 0.0;
-          const double udu2 = gsum((ok && lg > 0) ? zi * oi : 0.0, G);
-          const double o0 = __shfl_sync(0xffffffffu, oi, src);
-          if (ok) dp[j0 + lg] = soc_entry(code, lg, nu, t0, zi, oi, o0, udu2);
+        // SOC blocks of dim <= 32 (cones.py:740-764 applied twice) in four
+        // balanced phases: per-block sums by a thread per block, per-row
+        // entries by a thread per row (Y row -> block from the meta blob)
+        double *sU = reinterpret_cast<double *>(const_cast<unsigned char *>(smb) + a.o_scr);
+        double *sA = sU + a.bl.bmax, *sB = sA + a.bl.bmax;
+        const EBlk *bl = V.blks();
+        const uint16_t *rbk = V.rowblk();
+        for (int k = u.blk0 + (tid - u.blk0 % nt + nt) % nt; k < u.blk1; k += nt) {   // udu = z[1:]'t[1:]
+          const EBlk b = bl[k];
+          double s = 0.0;
+          for (int i = 1; i < b.dim; ++i) s += zY[b.j0 + i] * tval(b.j0 + i);
+          sU[k] = s;
+          sA[k] = tval(b.j0);  // dt
+        }
+        __syncthreads();
+        for (int j = u.row0 + (tid - u.row0 % nt + nt) % nt; j < u.row1; j += nt) {  // o = fin_row(D Pi t)
+          const int k = rbk[j];
+          const int i = j - bl[k].j0;
+          const double t0 = zY[bl[k].j0];
+          fin_row(j, soc_entry(scode[k], i, snu[k], t0, zY[j], tval(j), sA[k], sU[k]));
+        }
+        __syncthreads();
+        for (int k = u.blk0 + (tid - u.blk0 % nt + nt) % nt; k < u.blk1; k += nt) {   // udu2 = z[1:]'o[1:]
+          const EBlk b = bl[k];
+          double s = 0.0;
+          for (int i = 1; i < b.dim; ++i) s += zY[b.j0 + i] * outY[b.j0 + i];
+          sB[k] = s;
+        }
+        __syncthreads();
+        for (int j = u.row0 + (tid - u.row0 % nt + nt) % nt; j < u.row1; j += nt) {  // dp = D Pi o
+          const int k = rbk[j];
+          const int j0 = bl[k].j0;
+          dp[j] = soc_entry(scode[k], j - j0, snu[k], zY[j0], zY[j], outY[j], outY[j0], sB[k]);
         }
       } else {
         // large SOC blocks: a warp per block (soc_apply_warp), t in place in rs
@@ -497,6 +529,7 @@ __device__ __forceinline__ void eng_epilogue(const Mats &M, const EngArgs &a, co
       }
     }
   }
+  if (tp && KIND == STEP_FT) prof[9] += (unsigned long long)(clock64() - t0c);  // Y cone blocks
   warp_partials(acc, red, slot_mask<KIND>(upd));
 }
 
@@ -519,7 +552,7 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
   uint16_t *resc = V.resc();
   if (tid == 0) {
     mbar_init(&S.mbar, 1);
-    for (int k = 0; k < 8; ++k) S.prof[k] = 0;
+    for (int k = 0; k < 10; ++k) S.prof[k] = 0;
   }
   __syncthreads();
   uint32_t mphase = 0;
@@ -539,7 +572,7 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
     const int p = S.p;
     if (p >= a.B) {
       if (prof)
-        for (int k = 0; k < 8; ++k) atomicAdd(a.prof + k, S.prof[k]);
+        for (int k = 0; k < 10; ++k) atomicAdd(a.prof + k, S.prof[k]);
       return;
     }
     if (prof) t_mark = clock64();
@@ -631,13 +664,14 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
           }
           __syncwarp();
         }
-        eng_spmv<KU>(V, n, sv, dp, rs);
+        eng_spmv<KU>(V, n, m, sv, dp, rs);
         if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
         tick(1);
         if (!L.active) break;  // fin V stopped the solve (non-finite)
         // ---- B_u (+ the deferred update of the previous iteration)
-        eng_epilogue<KU>(M, a, V, g, E, sv, su, rs, dp, L.s_in, L.c_out, L.itn > 0, L, S.red);
+        eng_epilogue<KU>(M, a, V, g, E, sv, su, rs, dp, L.s_in, L.c_out, L.itn > 0, L, S.red,
+                         a.prof ? S.prof : nullptr);
         __syncthreads();
         tick(2);
         // ---- A_v || stop test + fin U
@@ -657,13 +691,14 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
           }
           __syncwarp();
         }
-        eng_spmv<KV>(V, n, su, dp, rs);
+        eng_spmv<KV>(V, n, m, su, dp, rs);
         if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
         tick(3);
         if (!L.active) break;  // the stop test ended the solve
         // ---- B_v (a zero beta skips the v-step: fin V keeps v)
-        if (!L.skip_v) eng_epilogue<KV>(M, a, V, g, E, su, sv, rs, dp, L.s_in, L.c_out, false, L, S.red);
+        if (!L.skip_v)
+          eng_epilogue<KV>(M, a, V, g, E, su, sv, rs, dp, L.s_in, L.c_out, false, L, S.red, a.prof ? S.prof : nullptr);
         pending_v = true;
         __syncthreads();
         tick(4);
@@ -754,9 +789,11 @@ __global__ void k_engine_meta(Mats M, BlobLayout bl, int res_cap, unsigned char 
     e.blk1 = u.blk1 - kb0;
     un[ui - yu0] = e;
   }
+  uint16_t *rb = reinterpret_cast<uint16_t *>(b + bl.o_rowblk);
   for (int k = kb0 + threadIdx.x; k < kb1; k += blockDim.x) {
     const BlockInfo bi = M.dpi.blk[k];
     bk[k - kb0] = EBlk{(int32_t)bi.param, (uint16_t)(bi.row - yo), (uint16_t)bi.dim};
+    for (int i = 0; i < bi.dim; ++i) rb[bi.row - yo + i] = (uint16_t)(k - kb0);
   }
   if (threadIdx.x == 0) {
     EngHead h{};
@@ -810,11 +847,13 @@ static size_t engine_offsets(const Handle &H, int bmax, EngArgs *a) {
   const size_t onu = o; o += sizeof(double) * bmax;
   const size_t ocode = o; o += sizeof(int) * bmax;
   o = al16(o);
+  const size_t oscr = o; o += 3 * sizeof(double) * bmax;   // per-block udu, dt, udu2 scratch
+  o = al16(o);                                               // blob: cp.async.bulk destination
   if (a) {
     a->nmax = nmax;
     a->mmax = mmax;
     a->o_q = (int)oq; a->o_px = (int)opx; a->o_b = (int)ob; a->o_z = (int)oz;
-    a->o_nu = (int)onu; a->o_code = (int)ocode; a->o_blob = (int)o;
+    a->o_nu = (int)onu; a->o_code = (int)ocode; a->o_scr = (int)oscr; a->o_blob = (int)o;
   }
   return o;
 }
@@ -839,7 +878,9 @@ static BlobLayout engine_blob_layout(const Handle &H) {
     umax = std::max(umax, (int)(y1 - y0));
     if (y1 > y0) bmax = std::max(bmax, H.cones.units[y1 - 1].blk1 - H.cones.units[y0].blk0);
   }
-  return blob_layout(smax, umax, bmax);
+  int nmax, mmax;
+  engine_dims(H, nmax, mmax);
+  return blob_layout(smax, umax, bmax, mmax);
 }
 
 static int engine_res_cap(const Handle &H, size_t blob_stride) {
@@ -962,21 +1003,21 @@ void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st) {
   QG_CUDA(cudaMemsetAsync(W.d_claim, 0, sizeof(int), st));
   static const bool want_prof = std::getenv("QG_ENG_PROF") != nullptr;
   if (want_prof) {
-    if (!H.eng_prof) H.eng_prof = dev_alloc<unsigned long long>(8);
-    QG_CUDA(cudaMemsetAsync(H.eng_prof, 0, 8 * sizeof(unsigned long long), st));
+    if (!H.eng_prof) H.eng_prof = dev_alloc<unsigned long long>(10);
+    QG_CUDA(cudaMemsetAsync(H.eng_prof, 0, 10 * sizeof(unsigned long long), st));
     a.prof = H.eng_prof;
   }
   kern<<<grid, nt, smem, st>>>(M, a);
   QG_LAUNCHED();
   if (want_prof) {
-    unsigned long long h[8];
+    unsigned long long h[10];
     QG_CUDA(cudaMemcpyAsync(h, H.eng_prof, sizeof(h), cudaMemcpyDeviceToHost, st));
     QG_CUDA(cudaStreamSynchronize(st));
     const double it = (double)std::max<unsigned long long>(h[5], 1);
     std::fprintf(stderr, "[qg engine] grid %d x %d thr, smem %zu B, res_cap %d | cycles/iter: A_u %.0f B_u %.0f "
-                 "A_v %.0f B_v %.0f | fin %.0f x2, spmv(warp 1) %.0f x2 | setup/problem %.0f | iters %llu\n", grid, nt,
-                 smem, a.res_cap, h[1] / it, h[2] / it, h[3] / it, h[4] / it, h[6] / it / 2, h[7] / it / 2,
-                 h[0] / (double)H.B, h[5]);
+                 "A_v %.0f B_v %.0f | fin %.0f x2, spmv(warp 1) %.0f x2 | F' epilogue rows %.0f, F' cone blocks %.0f | "
+                 "setup/problem %.0f | iters %llu\n", grid, nt, smem, a.res_cap, h[1] / it, h[2] / it, h[3] / it,
+                 h[4] / it, h[6] / it / 2, h[7] / it / 2, h[8] / it, h[9] / it, h[0] / (double)H.B, h[5]);
   }
 }
 

@@ -391,7 +391,8 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
 // the launch's tail.
 template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
-  const int ui = (KIND == STEP_FT && M.ft_order) ? M.ft_order[blockIdx.x] : (int)blockIdx.x;
+  // (an X_FINISH launch covers only the X units: natural order)
+  const int ui = (KIND == STEP_FT && M.ft_order && a.xmode != X_FINISH) ? M.ft_order[blockIdx.x] : (int)blockIdx.x;
   step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, ui);
 }
 

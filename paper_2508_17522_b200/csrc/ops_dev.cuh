@@ -69,6 +69,7 @@ __device__ __forceinline__ void sell_dot2(const SellView &S, int64_t sa, int64_t
     const int64_t pa = oa + 32LL * k, pb = ob + 32LL * k;
     const double va = ld_stream(S.val + pa), vb = ld_stream(S.val + pb);
     const int ca = ld_stream(colp + pa), cb = ld_stream(colp + pb);
+    QG_CHECK(ca >= 0 && cb >= 0);
     a += va * vec[ca];
     b += vb * vec[cb];
   }

@@ -143,6 +143,23 @@ void *pinned_staging(size_t bytes, int slot);
 // waits (pdl_wait) before its first read of data produced by the previous
 // kernel, and lets the next one start (pdl_trigger) once its main work is
 // issued.  Both are no-ops for ordinary launches.
+// Device-side invariant checks of a QG_CHECKS=1 build (index bounds of the
+// gathers, slice rows, resident plans, block tables): a violated check traps
+// (the kernel fails with an error the host reports), so the GPU test suite
+// run against that build is a bounds / consistency sanitizer.  Compiled out
+// of the production library.  (compute-sanitizer is not available on the
+// GPU pool.)
+#if defined(QG_CHECKS) && QG_CHECKS
+#define QG_CHECK(cond)         \
+  do {                         \
+    if (!(cond)) __trap();     \
+  } while (0)
+#else
+#define QG_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
