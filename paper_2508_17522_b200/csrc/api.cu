@@ -971,6 +971,20 @@ int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stre
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   *avg_ms = (double)ms / std::max(reps, 1);
+  if (which == 1 && H.cones.max_psd_order > 0 && std::getenv("QG_PSD_PROF")) {
+    // one more F' launch with the PSD units' phase clocks (diagnostics)
+    unsigned long long *d = dev_alloc<unsigned long long>(5), h5[5];
+    QG_CUDA(cudaMemsetAsync(d, 0, sizeof(h5), st));
+    StepArgs a{W.u, W.dpu, W.v, W.v, W.dpv, W.tY, W.tY2, W.st, 0, W.part};
+    a.prof = d;
+    launch_step(H, M, STEP_FT, a, st);
+    QG_CUDA(cudaMemcpyAsync(h5, d, sizeof(h5), cudaMemcpyDeviceToHost, st));
+    QG_CUDA(cudaStreamSynchronize(st));
+    dev_free(d);
+    const double u = (double)std::max<unsigned long long>(h5[0], 1);
+    std::fprintf(stderr, "[qg psd] %llu PSD units, cycles per unit: SpMV pass %.0f | D Pi t %.0f | rows %.0f | "
+                 "D Pi o %.0f\n", h5[0], h5[1] / u, h5[2] / u, h5[3] / u, h5[4] / u);
+  }
   QG_API_END
 }
 

@@ -243,6 +243,7 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
   const Embed E = M.emb[p];                            // (also preparation-time)
   if (KIND == STEP_FT && !isx && QG_PSD_PREFETCH) psd_prefetch_v(M.dpi, u, sm);  // V behind the SpMV pass
   pdl_wait();  // the previous kernel's vectors / LSMR state are complete past this point
+  const long long a_t0 = (a.prof != nullptr && threadIdx.x == 0) ? clock64() : 0;
   const double wN = a.in[M.NX + M.NY + p];             // issued with the LSMR-state loads below
   double s_in, c_out;
   if (!lsmr_runs(a, p, s_in, c_out)) {  // CTA-uniform
@@ -370,10 +371,24 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
         soc_epilogue(M.dpi, u, tY, fin_row, outY, a.dpout);
       } else {
         // generic path (PSD blocks, very large SOC blocks): CTA-wide phases
+        // (a.prof: QG_PSD_PROF diagnostics -- SM cycles of a PSD unit's
+        // phases: [units, SpMV pass, D Pi t, rows, D Pi o])
+        const bool tp = a.prof != nullptr && threadIdx.x == 0 && u.cls == CLS_PSD;
+        long long t1 = tp ? clock64() : 0;
         dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, sm, QG_PSD_PREFETCH && u.cls == CLS_PSD);
+        long long t2 = tp ? clock64() : 0;
         for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
         __syncthreads();
+        long long t3 = tp ? clock64() : 0;
         if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, sm, true);  // V still in sm
+        if (tp) {
+          const long long t4 = clock64();
+          atomicAdd(a.prof + 0, 1ULL);
+          atomicAdd(a.prof + 1, (unsigned long long)(t1 - a_t0));
+          atomicAdd(a.prof + 2, (unsigned long long)(t2 - t1));
+          atomicAdd(a.prof + 3, (unsigned long long)(t3 - t2));
+          atomicAdd(a.prof + 4, (unsigned long long)(t4 - t3));
+        }
       }
     }
   }

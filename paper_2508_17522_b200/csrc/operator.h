@@ -47,6 +47,7 @@ struct StepArgs {
   // rank-one term of the refine Jacobian J = F - r e_N' (testkit.py:443-451):
   // F step out -= r w_N ; F' step T out -= r'w (dot partial in slot 3)
   const double *rk1 = nullptr;
+  unsigned long long *prof = nullptr;  // QG_PSD_PROF diagnostics (qg_time_kernel): PSD unit phase cycles
 };
 
 struct UpdArgs {
