@@ -258,6 +258,9 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     order.reserve(H.nxu() + H.nyu());
     for (int u = 0; u < H.nyu(); ++u)
       if (H.cones.units[u].cls == CLS_PSD) order.push_back(H.nxu() + u);
+    H.n_psd_units = (int)order.size();
+    const char *split_env = std::getenv("QG_PSD_SPLIT");
+    H.psd_split = !split_env || std::atoi(split_env) != 0;
     for (int u = 0; u < H.nxu(); ++u) order.push_back(u);
     for (int u = 0; u < H.nyu(); ++u)
       if (H.cones.units[u].cls != CLS_PSD) order.push_back(H.nxu() + u);
@@ -481,8 +484,10 @@ static int kernels_per_iter(const Handle &H) {
   // k_step<F>, k_step<F'> (one carries the deferred update), 2 x k_fin;
   // row-partitioned: each step is X_PARTIAL + X_FINISH and each finalize is
   // k_part_reduce + k_fin (the NCCL kernels are not ours)
-  if (H.comm) return 8 - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
-  return 4 - (H.nxu() + H.nyu() == 0 ? 2 : 0);
+  // (+1: the F' step's PSD units as k_step_psd)
+  const int psd = psd_split(H) ? 1 : 0;
+  if (H.comm) return 8 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
+  return 4 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {

@@ -109,17 +109,20 @@ __device__ __forceinline__ void dmma_8x8x4(double &c0, double &c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <class FO>
+template <int TPW = 4, class FO>
 __device__ __forceinline__ void mm_dmma(int nt, bool lower, const double *A, int ai, int ak, const double *B, int bk,
                                         int bj, FO out) {
+  // TPW: output tiles per warp and pass (independent accumulator chains);
+  // 128-thread CTAs use 4 (16 tiles of a 32 x 32 product in one pass), the
+  // 256-thread PSD step 2 (one pass over 8 warps, half the chain per warp)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   const int fr = lane >> 2, fc = lane & 3;
   const int ntile = lower ? nt * (nt + 1) / 2 : nt * nt;
-  for (int t0 = warp * 4; t0 < ntile; t0 += nw * 4) {
-    int ti[4], tj[4];
-    double c0[4], c1[4];
+  for (int t0 = warp * TPW; t0 < ntile; t0 += nw * TPW) {
+    int ti[TPW], tj[TPW];
+    double c0[TPW], c1[TPW];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < TPW; ++q) {
       int t = t0 + q, i = 0;
       if (lower) {
         while (t > i) t -= ++i;  // row-major lower-triangle enumeration
@@ -133,7 +136,7 @@ __device__ __forceinline__ void mm_dmma(int nt, bool lower, const double *A, int
     }
     for (int k = 0; k < nt * 8; k += 4) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < TPW; ++q)
         if (ti[q] >= 0) {
           const double a = A[(ti[q] * 8 + fr) * ai + (k + fc) * ak];
           const double b = B[(k + fc) * bk + (tj[q] * 8 + fr) * bj];
@@ -141,7 +144,7 @@ __device__ __forceinline__ void mm_dmma(int nt, bool lower, const double *A, int
         }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
+    for (int q = 0; q < TPW; ++q)
       if (ti[q] >= 0) {
         out(ti[q] * 8 + fr, tj[q] * 8 + 2 * fc, c0[q]);
         out(ti[q] * 8 + fr, tj[q] * 8 + 2 * fc + 1, c1[q]);
@@ -206,8 +209,11 @@ static __device__ __forceinline__ void psd_prefetch_v(const DpiView &dv, const U
 // 3 instead of 4 matrices -> more CTAs per SM for the whole F' step).
 // have_v: V is already in sm from the previous apply of the same block (the
 // F' epilogue applies D Pi twice per block; no product writes V).
-static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
-                                     double *sm, bool have_v = false) {
+// Core with svec accessors: in(k) returns entry k of the input, out(k, v)
+// stores entry k of the result (global or shared memory); TPW as mm_dmma.
+template <int TPW, class FI, class FO>
+static __device__ void psd_apply_core(const double *Vg, const double *Bg, int d, FI in, FO out, double *sm,
+                                      bool have_v) {
   const int dp = psd_pad(d), ld = psd_ld(dp), sz = dp * ld;
   double *V = sm, *S = sm + sz, *T = sm + 2 * sz, *W = S;
   if (have_v) asm volatile("cp.async.wait_all;" ::: "memory");  // psd_prefetch_v (barrier below)
@@ -218,7 +224,7 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
     double s = 0.0;
     if (in_d) {
       const int a = i >= j ? i : j, b = i >= j ? j : i;
-      const double v = in[svec_index(a, b, d)];
+      const double v = in(svec_index(a, b, d));
       s = (a == b) ? v : v / kSqrt2;
     }
     S[i + j * ld] = s;
@@ -229,9 +235,9 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
   const int nt = dp >> 3;
   // T = S V ; W = (V' T) o B (lower, mirrored) ; T = V W ; out = svec(T V')
   // (padded rows / columns of every product are zero; only W and out filter)
-  mm_dmma(nt, false, S, 1, ld, V, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
+  mm_dmma<TPW>(nt, false, S, 1, ld, V, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
-  mm_dmma(nt, true, V, ld, 1, T, 1, ld, [&](int i, int j, double c) {
+  mm_dmma<TPW>(nt, true, V, ld, 1, T, 1, ld, [&](int i, int j, double c) {
     if (i >= j && i < d) {
       const double w = Bg[i + j * d] * c;
       W[i + j * ld] = w;
@@ -239,10 +245,10 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
     }
   });
   __syncthreads();
-  mm_dmma(nt, false, V, 1, ld, W, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
+  mm_dmma<TPW>(nt, false, V, 1, ld, W, 1, ld, [&](int i, int j, double c) { T[i + j * ld] = c; });
   __syncthreads();
-  mm_dmma(nt, true, T, 1, ld, V, ld, 1, [&](int i, int j, double c) {
-    if (i >= j && i < d) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
+  mm_dmma<TPW>(nt, true, T, 1, ld, V, ld, 1, [&](int i, int j, double c) {
+    if (i >= j && i < d) out(svec_index(i, j, d), (i == j) ? c : c * kSqrt2);
   });
   __syncthreads();
 #else
@@ -267,10 +273,25 @@ static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, 
   // out = svec(T V') on the lower triangle
   mm_tiles<PSD_TI, PSD_TJ>(d, true, [&](int i, int k) { return T[i + k * ld]; }, [&](int k, int j) { return V[j + k * ld]; },
                  [&](int i, int j, double c) {
-                   if (i >= j) out[svec_index(i, j, d)] = (i == j) ? c : c * kSqrt2;
+                   if (i >= j) out(svec_index(i, j, d), (i == j) ? c : c * kSqrt2);
                  });
   __syncthreads();
 #endif
+}
+
+static __device__ void psd_apply_cta(const double *Vg, const double *Bg, int d, const double *in, double *out,
+                                     double *sm, bool have_v = false) {
+  psd_apply_core<4>(Vg, Bg, d, [&](int k) { return in[k]; }, [&](int k, double v) { out[k] = v; }, sm, have_v);
+}
+
+// Shared-memory words of psd_apply_core for order d (V, S = W, T).
+static __host__ __device__ __forceinline__ int psd_core_words(int d) {
+#if QG_PSD_DMMA
+  const int dp = (d + 7) & ~7, ld = dp + 4;
+#else
+  const int dp = (d + 3) & ~3, ld = dp + 1;
+#endif
+  return 3 * dp * ld;
 }
 
 // Apply D Pi to the unit's rows.  in/out are indexed by (row - unit.row0);

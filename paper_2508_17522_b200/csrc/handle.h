@@ -95,6 +95,8 @@ struct Handle {
   int64_t *d_xoff = nullptr, *d_yoff = nullptr;
   int64_t *d_xunit_ptr = nullptr, *d_yunit_ptr = nullptr;
   int32_t *d_ft_order = nullptr;  // F' CTA -> unit order, PSD units first (null: natural order)
+  int n_psd_units = 0;            // leading PSD units of d_ft_order (their own F' kernel, k_step_psd)
+  bool psd_split = true;         // QG_PSD_SPLIT at creation (0: PSD units stay in k_step, A/B)
   double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;
   double *Pxbar = nullptr;
   Embed *emb = nullptr;

@@ -67,15 +67,12 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
                                          int64_t b1, int64_t b2, RowFn row) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   if (u.mode == MODE_SELL) {
-    // warps claim pairs of slices dynamically (balances uneven units)
-    __shared__ int next_slice;
-    if (threadIdx.x == 0) next_slice = u.s0;
-    __syncthreads();
-    while (true) {
-      int s = 0;
-      if (lane == 0) s = atomicAdd(&next_slice, QG_SLICE_CLAIM);
-      s = __shfl_sync(0xffffffffu, s, 0);
-      if (s >= u.s1) break;
+    // warps take pairs of slices in a fixed round-robin order: every row goes
+    // to the same thread on every run, so the row callbacks' partial sums are
+    // bit-reproducible (dynamic claims through a shared-memory counter made
+    // them depend on warp timing)
+    const int nw = (int)(blockDim.x >> 5);
+    for (int s = u.s0 + warp * QG_SLICE_CLAIM; s < u.s1; s += nw * QG_SLICE_CLAIM) {
       const int sb = (QG_SLICE_CLAIM == 2 && s + 1 < u.s1) ? s + 1 : -1;
       const int ra = rowof[(int64_t)s * 32 + lane];
       const int rb = sb >= 0 ? rowof[(int64_t)sb * 32 + lane] : -1;
@@ -411,6 +408,108 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
   step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, ui);
 }
 
+// F' step of the PSD units (one PSD block each), launched on a forked stream
+// beside the k_step<F'> launch of every other unit (launch_step_one): the two
+// D Pi applications of 4 dense products each make these the longest CTAs of
+// the step, so they get 256 threads (half the per-warp product chain of the
+// 128-thread step CTA, twice the SpMV lanes) and keep the whole epilogue in
+// shared memory -- t, w and old are staged there by the SpMV pass, D Pi t and
+// the row outputs never leave the CTA (the generic k_step path round-trips
+// them through the global tY / tY2 scratch).  The other units' launch then
+// needs no dynamic shared memory (more CTAs per SM, L1 left to the gathers).
+// Same expressions as step_unit's F' Y side; the unit's partials are summed
+// over a fixed row -> thread mapping (deterministic).
+constexpr int kPsdThreads = 256;
+template <int FEAT>
+__global__ void __launch_bounds__(kPsdThreads) k_step_psd(Mats M, StepArgs a) {
+  constexpr bool kWide = (FEAT & kFeatWide) != 0;
+  const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
+  extern __shared__ double sm[];
+  __shared__ double red[kWarps * kSlots];
+  const int ui = M.ft_order[blockIdx.x];  // PSD units lead the F' order
+  const Unit u = M.yu[ui - M.nxu];         // preparation-time data: before the PDL wait
+  const int p = u.prob;
+  const Embed E = M.emb[p];
+  const BlockInfo blk = M.dpi.blk[u.blk0];
+  const int d = blk.order, dim = u.row1 - u.row0;
+  const double *Vg = M.dpi.psd + blk.param, *Bg = Vg + d * d;
+  QG_CHECK(u.cls == CLS_PSD && u.blk1 == u.blk0 + 1 && blk.row == u.row0 && dim == d * (d + 1) / 2);
+  psd_prefetch_v(M.dpi, u, sm);
+  pdl_wait();
+  const bool tp = a.prof != nullptr && threadIdx.x == 0;
+  const long long t0 = tp ? clock64() : 0;
+  const double wN = a.in[M.NX + M.NY + p];
+  double s_in, c_out;
+  if (!lsmr_runs(a, p, s_in, c_out)) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  double *ts = sm + psd_core_words(d), *ws = ts + dim, *os = ws + dim;  // svec-indexed staging
+  const double *inX = a.in, *inY = a.in + M.NX;
+  const double *oldY = a.old ? a.old + M.NX : nullptr;
+  double *outY = a.out + M.NX;
+  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
+  const Lsmr *L = a.st ? a.st + p : nullptr;
+  if (a.upd_h && L && L->itn > 0) {  // deferred vector update (as step_unit)
+    const double c1 = L->c_hbar, c2 = L->c_x, c3 = L->c_h, sv = L->s_v;
+    for (int64_t r = M.NX + u.row0 + threadIdx.x; r < M.NX + u.row1; r += blockDim.x) {
+      const double hb = a.upd_h[r] - c1 * a.upd_hb[r];
+      const double x = a.upd_x[r] + c2 * hb;
+      a.upd_h[r] = a.in[r] * sv - c3 * a.upd_h[r];
+      a.upd_hb[r] = hb;
+      a.upd_x[r] = x;
+      acc[3] += x * x;
+    }
+  }
+  // pass 1: t = (A w1 - w_N b) - w2, w2 and old staged by row
+  for_rows<kWide, QG_FT_UNROLL, QG_ROWS32_FT, QG_ROWSG_FT>(
+      u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr, nullptr, inX, nullptr, u.lanes,
+      M.xoff[p], 0, [&](int r, double s, double) {
+        const int o = r - u.row0;
+        const double w = inY[r];
+        ts[o] = (s - wN * M.b[r]) - w;
+        ws[o] = w;
+        os[o] = c_out != 0.0 ? oldY[r] : 0.0;
+      });
+  __syncthreads();
+  const long long t1 = tp ? clock64() : 0;
+  // D Pi t (in place: the input is read into S before the result is written)
+  psd_apply_core<2>(Vg, Bg, d, [&](int k) { return ts[k]; }, [&](int k, double v) { ts[k] = v; }, sm, true);
+  const long long t2 = tp ? clock64() : 0;
+  // rows: o = s_in (D Pi t + w2)/z_N - c_out old
+  for (int o = threadIdx.x; o < dim; o += blockDim.x) {
+    const int r = u.row0 + o;
+    const double w = ws[o];
+    const double v = s_in * ((ts[o] + w) / E.zN) - (c_out != 0.0 ? c_out * os[o] : 0.0);
+    outY[r] = v;
+    os[o] = v;
+    acc[0] += M.b[r] * w;
+    acc[2] += v * v;
+    if (kRk1) acc[3] += a.rk1[M.NX + r] * w;
+  }
+  __syncthreads();
+  const long long t3 = tp ? clock64() : 0;
+  // D Pi o for the next F step (V still in shared memory)
+  if (a.dpout) {
+    double *dp = a.dpout + u.row0;
+    psd_apply_core<2>(Vg, Bg, d, [&](int k) { return os[k]; }, [&](int k, double v) { dp[k] = v; }, sm, true);
+  }
+  if (tp) {
+    const long long t4 = clock64();
+    atomicAdd(a.prof + 0, 1ULL);
+    atomicAdd(a.prof + 1, (unsigned long long)(t1 - t0));
+    atomicAdd(a.prof + 2, (unsigned long long)(t2 - t1));
+    atomicAdd(a.prof + 3, (unsigned long long)(t3 - t2));
+    atomicAdd(a.prof + 4, (unsigned long long)(t4 - t3));
+  }
+  pdl_trigger();
+  double tot[kSlots];
+  cta_sum_slots(acc, red, tot);
+  if (threadIdx.x == 0 && a.part)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
+}
+
 // -------------------------------------------------------------- update --
 // hbar = h - c1 hbar ; x = x + c2 hbar ; h = v s_v - c3 h   (lsmr.py:142-144)
 __global__ void __launch_bounds__(kThreads) k_update(Mats M, UpdArgs a) {
@@ -720,10 +819,55 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a0, c
   launch_step_one(H, M, kind, a, st);
 }
 
-static void launch_step_one(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st) {
-  const unsigned grid = (unsigned)(a.xmode == X_FINISH ? H.nxu() : H.nxu() + H.nyu());
+// Per-host-thread side stream and fork / join events of the PSD F' launch
+// (thread-local: calls from different host threads never share an event).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  SideStream() {
+    QG_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    QG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    QG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
+};
+
+bool psd_split(const Handle &H) { return H.psd_split && H.n_psd_units > 0; }
+
+// k_step_psd's shared memory: psd_apply_core's matrices + t, w, old (svec).
+static size_t psd_step_smem(const Handle &H) {
+  const int d = H.cones.max_psd_order;
+  return ((size_t)psd_core_words(d) + 3 * (size_t)(d * (d + 1) / 2)) * sizeof(double);
+}
+
+static void launch_step_one(const Handle &H, const Mats &M0, int kind, const StepArgs &a, cudaStream_t st) {
+  unsigned grid = (unsigned)(a.xmode == X_FINISH ? H.nxu() : H.nxu() + H.nyu());
   if (grid == 0) return;
-  const size_t smem = step_smem(H);
+  size_t smem = step_smem(H);
+  Mats M = M0;
+  // F' with PSD blocks: the PSD units run as k_step_psd on a forked stream,
+  // the rest of the step as k_step (no PSD unit left: no dynamic smem).
+  // QG_PSD_SPLIT=0: every unit in k_step (A/B).
+  SideStream *side = nullptr;
+  if (kind == STEP_FT && a.xmode != X_FINISH && psd_split(H)) {
+    static thread_local SideStream ss;
+    side = &ss;
+    QG_CUDA(cudaEventRecord(side->fork, st));
+    QG_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+    const size_t psm = psd_step_smem(H);
+    const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
+    auto kp = feat == kFeatAll ? k_step_psd<kFeatAll> : (feat == kFeatWide ? k_step_psd<kFeatWide> : k_step_psd<0>);
+    if (psm > 48 * 1024) raise_dynamic_smem(reinterpret_cast<const void *>(kp), psm);
+    kp<<<(unsigned)H.n_psd_units, kPsdThreads, psm, side->s>>>(M0, a);
+    QG_LAUNCHED();
+    QG_CUDA(cudaEventRecord(side->join, side->s));
+    M.ft_order = M0.ft_order + H.n_psd_units;
+    grid -= (unsigned)H.n_psd_units;
+    smem = 0;
+  }
+  if (grid == 0) {
+    if (side) QG_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+    return;
+  }
   static int threads = 0;
   if (!threads) {  // QG_STEP_THREADS: A/B switch for the CTA size (32..128)
     const char *e = std::getenv("QG_STEP_THREADS");
@@ -758,6 +902,7 @@ static void launch_step_one(const Handle &H, const Mats &M, int kind, const Step
     else go(k_step<STEP_FT, 8, 0>, smem);
   }
   QG_LAUNCHED();
+  if (side) QG_CUDA(cudaStreamWaitEvent(st, side->join, 0));
 }
 
 void fin_ptrs(const Handle &H, FinArgs &a) {

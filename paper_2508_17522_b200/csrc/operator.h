@@ -59,6 +59,7 @@ struct UpdArgs {
 
 Mats make_mats(const Handle &H);
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
+bool psd_split(const Handle &H);  // F' PSD units run as their own kernel (k_step_psd) beside k_step
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
 void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole-problem handle
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);

@@ -219,3 +219,49 @@ def test_c5b_row_partitioned_operator(c5b, world):
     for k in range(2):
         got = np.concatenate([out[0][k][:n]] + [o[k][n:n + s.m] for o, s in zip(out, shards)] + [out[0][k][-1:]])
         assert gap(got, ref[k]) <= 1e-13
+
+
+def _c4_small(seed):
+    """c4's cone mix at 1/8 of its PSD blocks: nonneg + 64 x PSD(32), Gram P."""
+    cones = [("nonneg", 1250, 0, 0)] + [("psd", 528, 32, 0)] * 64
+    return synth.custom(cones, n=2500, nnzA=250_000, seed=seed, diag_P=False)
+
+
+def test_psd_split_kernel_matches_inline_path(monkeypatch):
+    """c4-shaped PSD handle: the F' step's PSD units as their own 256-thread
+    kernel (k_step_psd, default) against the same units inside k_step
+    (QG_PSD_SPLIT=0).  Same per-entry expressions and product tiles: the X
+    and Y outputs are bit-identical; the T entry (partial sums in another
+    order) agrees to ulp level; fixed-cap jvp / vjp at the P2 bound."""
+    bt = _c4_small(seed=5)
+    dirs = synth.directions(bt, seed=6)
+    monkeypatch.setenv("QG_PSD_SPLIT", "1")
+    b1 = _batch(bt)
+    monkeypatch.setenv("QG_PSD_SPLIT", "0")
+    b0 = _batch(bt)
+    NE = sum(bt.n) + sum(bt.m) + bt.B
+    w = _dev(np.random.default_rng(2).standard_normal(NE))
+    for t in (False, True):
+        o1 = b1.apply_F_device(w, transpose=t).cpu().numpy()
+        o0 = b0.apply_F_device(w, transpose=t).cpu().numpy()
+        assert np.array_equal(o1[:NE - bt.B], o0[:NE - bt.B]), t
+        assert gap(o1, o0) <= 1e-13
+    j1, v1 = _run(b1, dirs, 3)
+    j0, v0 = _run(b0, dirs, 3)
+    for a, c in zip(j1 + v1, j0 + v0):
+        assert gap(a, c) <= 1e-6
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5a"])
+def test_graph_path_bit_deterministic(monkeypatch, cfg):
+    """Repeated fixed-cap solves on the graph path (SELL units with dynamic
+    slice claims, the split PSD kernel) are bit-identical."""
+    monkeypatch.setenv("QG_ENGINE", "0")
+    monkeypatch.setenv("QG_SELL", "1")
+    bt = _c4_small(seed=7) if cfg == "c4" else synth.generate(cfg, seed=7, batch=8)
+    dirs = synth.directions(bt, seed=8)
+    b = _batch(bt)
+    r1 = _run(b, dirs, 20)
+    r2 = _run(b, dirs, 20)
+    for a, c in zip(r1[0] + r1[1], r2[0] + r2[1]):
+        assert np.array_equal(a, c)
