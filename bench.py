@@ -411,11 +411,14 @@ def run_ours(args):
         # F' launch time, against cuBLAS DGEMM measured here (a lower bound on
         # the PSD kernels' own rate, since the launch also streams the SpMVs)
         fp64 = _dgemm_tflops(dev)
-        ach_f = ab["FT_psd_flops"] / (t_ft / 1e3) / 1e12
-        roof["psd_fp64"] = {"achieved": round(ach_f, 3), "peak": round(fp64, 2), "unit": "TFLOP/s",
+        t_psd = b.time_kernel(3, reps=20)  # k_step_psd alone: the PSD units' own time
+        ach_f = ab["FT_psd_flops"] / (t_psd / 1e3) / 1e12
+        roof["psd_fp64"] = {"kernel": "k_step_psd (PSD units of the F' step: SpMV pass + 2 D Pi applications "
+                                      "of 4 dense products each, timed alone)",
+                            "achieved": round(ach_f, 3), "peak": round(fp64, 2), "unit": "TFLOP/s",
                             "peak_source": "cuBLAS DGEMM 8192^3 fp64, measured in this run",
                             "frac": round(ach_f / fp64, 4), "flops_per_launch": ab["FT_psd_flops"],
-                            "products": "mma.sync m8n8k4 f64 (DMMA)"}
+                            "launch_ms": round(t_psd, 4), "products": "mma.sync m8n8k4 f64 (DMMA)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # contract: N=1 only
@@ -497,6 +500,10 @@ def _traffic_fields(t):
     return {"traffic": t["bytes"] if t else None, "traffic_detail": t}
 
 
+def _has_psd(cfg):
+    return cfg == "c4"
+
+
 def _traffic(cfg, alg, kernel="k_step", batch=None):
     """DRAM bytes (read + write) per launch of the dominant kernel, captured
     IN THIS RUN: tools/traffic_probe.py rebuilds this workload and runs the
@@ -508,10 +515,13 @@ def _traffic(cfg, alg, kernel="k_step", batch=None):
 
     ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu" if os.path.exists("/usr/local/cuda/bin/ncu") else None)
     if ncu and not os.environ.get("QG_NO_NCU"):
+        # an F' step of a batch with PSD blocks is two kernels (k_step over the
+        # other units, k_step_psd beside it): both launches of one step
+        nk = 2 if (kernel != "k_engine" and _has_psd(cfg)) else 1
         filt = ["-k", "regex:^k_engine$"] if kernel == "k_engine" else \
-            ["--kernel-name-base", "mangled", "-k", "regex:k_stepILi1"]
+            ["--kernel-name-base", "mangled", "-k", "regex:k_stepILi1|k_step_psd"]
         cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum", *filt,
-               "-c", "1", "--csv", sys.executable, os.path.join(ROOT, "tools", "traffic_probe.py"),
+               "-c", str(nk), "--csv", sys.executable, os.path.join(ROOT, "tools", "traffic_probe.py"),
                "--config", cfg, "--which", "engine" if kernel == "k_engine" else "ft"]
         if batch:
             cmd += ["--batch", str(batch)]
@@ -526,12 +536,12 @@ def _traffic(cfg, alg, kernel="k_step", batch=None):
                     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9,
                              "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1,
                              "s": 1}.get(unit, 1)
-                    vals[parts[-3]] = v * scale
+                    vals[parts[-3]] = vals.get(parts[-3], 0.0) + v * scale  # summed over the step's kernels
             if "dram__bytes_read.sum" in vals:
                 return {"bytes": int(vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0)),
                         "read": int(vals["dram__bytes_read.sum"]), "write": int(vals.get("dram__bytes_write.sum", 0)),
                         "ncu_duration_ms": round(vals.get("gpu__time_duration.sum", 0) * 1e3, 4),
-                        "source": f"ncu in this run ({kernel}, one launch, cold L2)"}
+                        "source": f"ncu in this run ({'k_step + k_step_psd, one F' + chr(39) + ' step' if nk == 2 else kernel + ', one launch'}, cold L2, serialised)"}
         except (OSError, subprocess.SubprocessError, ValueError):
             pass
     path = os.path.join(ROOT, "profiles", "traffic.json")

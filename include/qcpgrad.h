@@ -161,7 +161,8 @@ int qg_spmv_csc(int64_t nrows, int64_t ncols, const int64_t *col_ptr, const int6
 
 /* Benchmark hook: launch one hot-path kernel of the prepared batch -- which =
  * 0: fused F step (SpMV + epilogue), 1: fused F' step (SpMV + D Pi epilogues),
- * 2: LSMR vector update -- `reps` times on `stream` between CUDA events;
+ * 2: LSMR vector update, 3: the F' step's PSD units alone (k_step_psd; batches
+ * with PSD blocks) -- `reps` times on `stream` between CUDA events;
  * *avg_ms receives the mean device time per launch. */
 int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stream);
 

@@ -350,6 +350,8 @@ static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &
   sv.rk1 = rk1;
   fv = FinArgs{H.B, PH_STEP_V, kv, W.st, W.part, W.u, W.v, W.v, W.h, W.hb, W.x, W.v};
   fv.rk1 = rk1;
+  // each follows a step kernel, which never writes the LSMR state or T entries
+  fu.early = fv.early = 1;
 }
 
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
@@ -956,6 +958,10 @@ int qg_time_kernel(qg_handle *h, int which, int reps, double *avg_ms, void *stre
     } else if (which == 1) {
       StepArgs a{W.u, W.dpu, W.v, W.v, W.dpv, W.tY, W.tY2, W.st, 0, W.part};
       launch_step(H, M, STEP_FT, a, st);
+    } else if (which == 3) {
+      if (!psd_split(H)) throw Error{QG_ERR_VALIDATION, "qg_time_kernel: which = 3 needs PSD blocks"};
+      StepArgs a{W.u, W.dpu, W.v, W.v, W.dpv, W.tY, W.tY2, W.st, 0, W.part};
+      launch_step_psd(H, M, a, st);
     } else {
       UpdArgs ua{W.h, W.hb, W.x, W.v, W.st, W.part};
       launch_update(H, M, ua, st);

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a)
 // over a fixed row -> thread mapping (deterministic).
 constexpr int kPsdThreads = 256;
 template <int FEAT>
-__global__ void __launch_bounds__(kPsdThreads) k_step_psd(Mats M, StepArgs a) {
+__global__ void __launch_bounds__(kPsdThreads, 4) k_step_psd(Mats M, StepArgs a) {  // 4 CTAs/SM: 64 registers
   constexpr bool kWide = (FEAT & kFeatWide) != 0;
   const bool kRk1 = (FEAT & kFeatRk1) != 0 && a.rk1 != nullptr;
   extern __shared__ double sm[];
@@ -574,8 +574,23 @@ __device__ __forceinline__ bool fin_skips(const FinArgs &a, int p) {
 // loads and stores it cooperatively), else the state in global memory.
 // The scalar work is fin_core (lsmr_dev.cuh) on the T entries of the
 // vectors, loaded here and stored back where fin_core wrote them.
+// T entries of problem p a finalize of phase a.phase reads (lsmr_dev.cuh TVals).
+__device__ __forceinline__ TVals load_tvals(const Mats &M, const FinArgs &a, int p) {
+  const int64_t T = M.NX + M.NY + p;
+  TVals t;
+  t.in = a.in ? __ldcg(a.in + T) : 0.0;
+  t.old = a.old ? __ldcg(a.old + T) : 0.0;
+  t.out = t.old;
+  t.h = (a.phase == PH_STEP_V) ? __ldcg(a.h + T) : 0.0;
+  t.hb = (a.phase == PH_STEP_V) ? __ldcg(a.hb + T) : 0.0;
+  t.x = (a.phase == PH_STEP_V || a.phase == PH_STEP_U || a.phase == PH_STEP_X) ? __ldcg(a.x + T) : 0.0;
+  t.rk1 = a.rk1 ? __ldcg(a.rk1 + T) : 0.0;
+  return t;
+}
+
 __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int p, int lane,
-                                            const double *pre = nullptr, Lsmr *Lsh = nullptr) {
+                                            const double *pre = nullptr, Lsmr *Lsh = nullptr,
+                                            const TVals *tpre = nullptr) {
   Lsmr *L = Lsh ? Lsh : (a.st ? a.st + p : nullptr);
   if (fin_skips(a, p)) return;
   // deterministic per-problem sums of the producers' partials (fixed order)
@@ -597,14 +612,7 @@ __device__ __forceinline__ void fin_problem(const Mats &M, const FinArgs &a, int
   }
   if (lane != 0) return;
   const int64_t T = M.NX + M.NY + p;
-  TVals t;
-  t.in = a.in ? a.in[T] : 0.0;
-  t.old = a.old ? a.old[T] : 0.0;
-  t.out = t.old;
-  t.h = (a.phase == PH_STEP_V) ? a.h[T] : 0.0;
-  t.hb = (a.phase == PH_STEP_V) ? a.hb[T] : 0.0;
-  t.x = (a.phase == PH_STEP_V || a.phase == PH_STEP_U || a.phase == PH_STEP_X) ? a.x[T] : 0.0;
-  t.rk1 = a.rk1 ? a.rk1[T] : 0.0;
+  TVals t = tpre ? *tpre : load_tvals(M, a, p);
   const int w = fin_core(M.emb[p], a.phase, a.kind, L, sx, sy, t, a.rk1 != nullptr, true);
   if (w & TV_OUT) a.out[T] = t.out;
   if (w & TV_H) a.h[T] = t.h;
@@ -625,11 +633,7 @@ __global__ void k_fin(Mats M, FinArgs a) {
 // warp-per-problem version spent ~25 sequential L2 round trips per lane
 // summing c2's ~800 slots.
 __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
-  pdl_wait();
-  pdl_trigger();
   const int p = (int)blockIdx.x;
-  if (fin_skips(a, p)) return;  // CTA-uniform
-  __shared__ double red[(256 / 32) * 2 * kSlots];
   // the LSMR state goes to shared memory in one coalesced sweep (the scalar
   // recurrence then never waits on global memory for it), and back at the end
   constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
@@ -637,15 +641,27 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
   __shared__ unsigned long long sLw[kLw];
   Lsmr *Lsh = a.st ? reinterpret_cast<Lsmr *>(sLw) : nullptr;
   const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(a.st + p);
-  if (Lsh)
+  TVals tv{};
+  if (a.early) {
+    // loop finalizes (FinArgs::early): state and T entries issued ahead of
+    // the wait for the step kernel; L2 loads (cg): written by an earlier grid
+    if (Lsh)
+      for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = __ldcg(Lg + w);
+    if (threadIdx.x == 0) tv = load_tvals(M, a, p);
+  }
+  pdl_wait();
+  pdl_trigger();
+  if (!a.early && Lsh)
     for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = Lg[w];
+  if (fin_skips(a, p)) return;  // CTA-uniform
+  __shared__ double red[(256 / 32) * 2 * kSlots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   double s[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll 2
+#pragma unroll 4
   for (int64_t k = a.px_ptr[p] + threadIdx.x; k < a.px_ptr[p + 1]; k += blockDim.x)
 #pragma unroll
     for (int j = 0; j < kSlots; ++j) s[j] += __ldcg(a.px + k * kSlots + j);
-#pragma unroll 2
+#pragma unroll 4
   for (int64_t k = a.py_ptr[p] + threadIdx.x; k < a.py_ptr[p + 1]; k += blockDim.x)
 #pragma unroll
     for (int j = 0; j < kSlots; ++j) s[kSlots + j] += __ldcg(a.py + k * kSlots + j);
@@ -663,7 +679,7 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
       for (int w = 1; w < nw; ++w) t += red[w * 2 * kSlots + j];
       pre[j] = t;
     }
-    fin_problem(M, a, p, 0, pre, Lsh);
+    fin_problem(M, a, p, 0, pre, Lsh, a.early ? &tv : nullptr);
   }
   if (Lsh) {
     __syncthreads();
@@ -819,6 +835,13 @@ void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a0, c
   launch_step_one(H, M, kind, a, st);
 }
 
+// Kernel variant of a step: the CTA-per-row path and the rarely used
+// features run as their own instantiations (12 CTAs/SM): plain wide-row
+// handles get a lean variant, partitioned / rank-one steps the all-features one.
+static int step_feat(const Handle &H, const StepArgs &a) {
+  return (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
+}
+
 // Per-host-thread side stream and fork / join events of the PSD F' launch
 // (thread-local: calls from different host threads never share an event).
 struct SideStream {
@@ -839,35 +862,9 @@ static size_t psd_step_smem(const Handle &H) {
   return ((size_t)psd_core_words(d) + 3 * (size_t)(d * (d + 1) / 2)) * sizeof(double);
 }
 
-static void launch_step_one(const Handle &H, const Mats &M0, int kind, const StepArgs &a, cudaStream_t st) {
-  unsigned grid = (unsigned)(a.xmode == X_FINISH ? H.nxu() : H.nxu() + H.nyu());
-  if (grid == 0) return;
-  size_t smem = step_smem(H);
-  Mats M = M0;
-  // F' with PSD blocks: the PSD units run as k_step_psd on a forked stream,
-  // the rest of the step as k_step (no PSD unit left: no dynamic smem).
-  // QG_PSD_SPLIT=0: every unit in k_step (A/B).
-  SideStream *side = nullptr;
-  if (kind == STEP_FT && a.xmode != X_FINISH && psd_split(H)) {
-    static thread_local SideStream ss;
-    side = &ss;
-    QG_CUDA(cudaEventRecord(side->fork, st));
-    QG_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
-    const size_t psm = psd_step_smem(H);
-    const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
-    auto kp = feat == kFeatAll ? k_step_psd<kFeatAll> : (feat == kFeatWide ? k_step_psd<kFeatWide> : k_step_psd<0>);
-    if (psm > 48 * 1024) raise_dynamic_smem(reinterpret_cast<const void *>(kp), psm);
-    kp<<<(unsigned)H.n_psd_units, kPsdThreads, psm, side->s>>>(M0, a);
-    QG_LAUNCHED();
-    QG_CUDA(cudaEventRecord(side->join, side->s));
-    M.ft_order = M0.ft_order + H.n_psd_units;
-    grid -= (unsigned)H.n_psd_units;
-    smem = 0;
-  }
-  if (grid == 0) {
-    if (side) QG_CUDA(cudaStreamWaitEvent(st, side->join, 0));
-    return;
-  }
+// k_step over `grid` units (the unit order of M), on st with PDL.
+static void launch_step_main(const Handle &H, const Mats &M, int kind, const StepArgs &a, unsigned grid,
+                             size_t smem, cudaStream_t st) {
   static int threads = 0;
   if (!threads) {  // QG_STEP_THREADS: A/B switch for the CTA size (32..128)
     const char *e = std::getenv("QG_STEP_THREADS");
@@ -886,10 +883,7 @@ static void launch_step_one(const Handle &H, const Mats &M0, int kind, const Ste
     if (sm_bytes > 48 * 1024) raise_dynamic_smem(reinterpret_cast<const void *>(kern), sm_bytes);
     launch_pdl(kern, dim3(grid), dim3(threads), sm_bytes, st, M, a);
   };
-  // the CTA-per-row path and the rarely used features run as their own
-  // instantiations (12 CTAs/SM): plain wide-row handles get a lean variant,
-  // partitioned / rank-one steps the all-features one
-  const int feat = (H.comm || a.rk1) ? kFeatAll : (H.has_wide ? kFeatWide : 0);
+  const int feat = step_feat(H, a);
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
     else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
@@ -902,7 +896,37 @@ static void launch_step_one(const Handle &H, const Mats &M0, int kind, const Ste
     else go(k_step<STEP_FT, 8, 0>, smem);
   }
   QG_LAUNCHED();
-  if (side) QG_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+}
+
+void launch_step_psd(const Handle &H, const Mats &M, const StepArgs &a, cudaStream_t st) {
+  const size_t psm = psd_step_smem(H);
+  const int feat = step_feat(H, a);
+  auto kp = feat == kFeatAll ? k_step_psd<kFeatAll> : (feat == kFeatWide ? k_step_psd<kFeatWide> : k_step_psd<0>);
+  if (psm > 48 * 1024) raise_dynamic_smem(reinterpret_cast<const void *>(kp), psm);
+  kp<<<(unsigned)H.n_psd_units, kPsdThreads, psm, st>>>(M, a);
+  QG_LAUNCHED();
+}
+
+static void launch_step_one(const Handle &H, const Mats &M0, int kind, const StepArgs &a, cudaStream_t st) {
+  const unsigned grid = (unsigned)(a.xmode == X_FINISH ? H.nxu() : H.nxu() + H.nyu());
+  if (grid == 0) return;
+  if (!(kind == STEP_FT && a.xmode != X_FINISH && psd_split(H))) {
+    launch_step_main(H, M0, kind, a, grid, step_smem(H), st);
+    return;
+  }
+  // F' with PSD blocks: the PSD units run as k_step_psd on a forked stream,
+  // the rest of the step as k_step (no PSD unit left: no dynamic smem).
+  // QG_PSD_SPLIT=0 at handle creation: every unit in k_step (A/B).
+  static thread_local SideStream side;
+  QG_CUDA(cudaEventRecord(side.fork, st));
+  QG_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
+  launch_step_psd(H, M0, a, side.s);
+  QG_CUDA(cudaEventRecord(side.join, side.s));
+  Mats M = M0;
+  M.ft_order = M0.ft_order + H.n_psd_units;
+  const unsigned rest = grid - (unsigned)H.n_psd_units;
+  if (rest) launch_step_main(H, M, kind, a, rest, 0, st);
+  QG_CUDA(cudaStreamWaitEvent(st, side.join, 0));
 }
 
 void fin_ptrs(const Handle &H, FinArgs &a) {

@@ -25,6 +25,10 @@ struct FinArgs {
   const double *px = nullptr, *py = nullptr;
   const int64_t *px_ptr = nullptr, *py_ptr = nullptr;
   const double *rk1 = nullptr;  // rank-one term (StepArgs::rk1), T entries read here
+  // LSMR loop finalizes: the LSMR state and the T entries come from EARLIER
+  // finalizes (the step kernel launched in between never writes them), so
+  // k_fin_cta loads them before its griddepcontrol.wait
+  int early = 0;
 };
 
 struct StepArgs {
@@ -60,6 +64,7 @@ struct UpdArgs {
 Mats make_mats(const Handle &H);
 void launch_step(const Handle &H, const Mats &M, int kind, const StepArgs &a, cudaStream_t st);
 bool psd_split(const Handle &H);  // F' PSD units run as their own kernel (k_step_psd) beside k_step
+void launch_step_psd(const Handle &H, const Mats &M, const StepArgs &a, cudaStream_t st);  // k_step_psd alone
 void launch_fin(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);
 void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole-problem handle
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);

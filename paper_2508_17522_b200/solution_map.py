@@ -230,7 +230,8 @@ class QCPBatch:
 
     def time_kernel(self, which, reps=20):
         """Mean device ms per launch of a hot kernel (0: F step, 1: F' step,
-        2: LSMR update), CUDA events on the current stream."""
+        2: LSMR update, 3: the F' step's PSD units alone), CUDA events on the
+        current stream."""
         ms = N.c_dbl()
         N.check(N.lib().qg_time_kernel(self._h, int(which), int(reps), N.ctypes.byref(ms), N.stream_ptr()))
         return float(ms.value)

@@ -26,7 +26,7 @@ for _ in range(2):
 spec = cones.ConeSpec([cones.ConeBlock.nonneg(10000)] + [cones.ConeBlock.psd(32)] * 512)
 m = sum(blk.dim for blk in spec.blocks)
 rng = np.random.default_rng(0)
-z = torch.from_numpy(rng.standard_normal(m)).cuda()
+z = rng.standard_normal(m)
 D = cones.ConeDerivative(spec, z, dual=True)
 dz = torch.from_numpy(rng.standard_normal(m)).cuda()
 for _ in range(3):
