@@ -44,6 +44,22 @@ def _ranges(o, lo, hi):
                 dx=(o["n"][lo], o["n"][hi]), dy=(o["m"][lo], o["m"][hi]), ds=(o["m"][lo], o["m"][hi]))
 
 
+def chunk_bounds(B, chunks):
+    """Problem ranges of the pipeline: a short first chunk (1/16 of the
+    batch, >= 148 problems: one per SM of the resident engine) so the one
+    upload nothing can hide behind is short, then equal chunks.  The first
+    chunk's kernels cover the second chunk's upload when the rest is cut into
+    chunks - 1 pieces of <= ~5x its size."""
+    chunks = max(int(chunks), 1)
+    if chunks == 1 or B < 2 * 148:
+        edges = [B * c // chunks for c in range(chunks + 1)]
+    else:
+        first = max(148, B // 16)
+        rest = B - first
+        edges = [0] + [first + rest * c // (chunks - 1) for c in range(chunks)]
+    return [e for i, e in enumerate(edges) if i == 0 or e > edges[i - 1]]
+
+
 def evaluate_host(n, m, P_nnz, A_nnz, blocks, data, dirs, *, chunks=4, atol=1e-10, btol=1e-10, max_iter=None,
                   out=None):
     """jvp and vjp of every problem of a host batch.
@@ -63,8 +79,7 @@ def evaluate_host(n, m, P_nnz, A_nnz, blocks, data, dirs, *, chunks=4, atol=1e-1
         out = {k: torch.empty(int(v), dtype=torch.float64, pin_memory=True) for k, v in shapes.items()}
     comp = torch.cuda.current_stream()
     copy = torch.cuda.Stream()
-    bounds = [B * c // max(chunks, 1) for c in range(max(chunks, 1) + 1)]
-    bounds = [b for i, b in enumerate(bounds) if i == 0 or b > bounds[i - 1]]
+    bounds = chunk_bounds(B, chunks)
     f64, i64 = torch.float64, torch.int64
     kw = dict(atol=atol, btol=btol, max_iter=max_iter)
 
