@@ -182,15 +182,10 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     QG_CUDA(cudaMemcpyAsync(H.AT.val, d.A_vals, sizeof(double) * H.noffA[B], cudaMemcpyDeviceToDevice, st));
   trace("transpose A");
 
-  // row-length statistics for the unit partition (pinned staging: DMA speed)
-  int32_t *rpP = static_cast<int32_t *>(pinned_staging(sizeof(int32_t) * (2 * (H.NX + 1) + H.NY + 1), 0));
-  int32_t *rpAT = rpP + (H.NX + 1), *rpA = rpAT + (H.NX + 1);
-  QG_CUDA(cudaMemcpyAsync(rpP, H.P.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
-  QG_CUDA(cudaMemcpyAsync(rpAT, H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
-  QG_CUDA(cudaMemcpyAsync(rpA, H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
-  QG_CUDA(cudaStreamSynchronize(st));
-  trace("rowptr D2H");
-  const int64_t nnzX = (int64_t)rpP[H.NX] + rpAT[H.NX], nnzY = rpA[H.NY];
+  // Unit sizes from host-known totals (the descriptor's nnz counts): the cone
+  // table's host passes then run while the transposes above are still on the
+  // GPU, before the row-pointer download synchronises the stream.
+  const int64_t nnzX = H.noffP[B] + H.noffA[B], nnzY = H.noffA[B];
   // aim for >= 4 CTAs per SM when the batch is large enough, 2k..16k entries per unit
   const int64_t total = nnzX + nnzY + H.NX + H.NY;
   // small problems get small units (all SMs busy, short per-warp chains),
@@ -199,6 +194,21 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   if (const char *e = std::getenv("QG_TARGET_NNZ")) target_nnz = std::max<int64_t>(64, std::atoll(e));  // A/B
   const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
   const int64_t target_rows_y = std::max<int64_t>(8, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
+
+  // cones and Y units
+  H.cones.build(d.blocks, d.nblocks, H.yoff, target_rows_y, st);
+  trace("cone table");
+
+  // row-length statistics for the unit partition (pinned staging: DMA speed)
+  int32_t *rpP = static_cast<int32_t *>(pinned_staging(sizeof(int32_t) * (2 * (H.NX + 1) + H.NY + 1), 0));
+  int32_t *rpAT = rpP + (H.NX + 1), *rpA = rpAT + (H.NX + 1);
+  QG_CUDA(cudaMemcpyAsync(rpP, H.P.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpAT, H.AT.rp, sizeof(int32_t) * (H.NX + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaMemcpyAsync(rpA, H.A.rp, sizeof(int32_t) * (H.NY + 1), cudaMemcpyDeviceToHost, st));
+  QG_CUDA(cudaStreamSynchronize(st));
+  trace("rowptr D2H");
+  if ((int64_t)rpP[H.NX] + rpAT[H.NX] != nnzX || rpA[H.NY] != nnzY)
+    throw Error{QG_ERR_VALIDATION, "sparse structure does not match the declared nnz counts"};
 
   // X units: nnz-balanced row ranges within each problem (problems in
   // parallel host chunks, concatenated in problem order)
@@ -233,9 +243,6 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   H.d_xunits = dev_alloc<Unit>(H.xunits.size());  // uploaded by build_sell with the modes
   trace("x units");
 
-  // cones and Y units
-  H.cones.build(d.blocks, d.nblocks, H.yoff, target_rows_y, st);
-  trace("cone table");
   H.engine = engine_candidate(H);
   build_sell(H, rpP, rpAT, rpA, H.engine, st);
   H.engine = H.engine && engine_units_ok(H);

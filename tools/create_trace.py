@@ -4,7 +4,8 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-os.environ["QG_TRACE"] = "1"
+if "notrace" not in sys.argv:  # `notrace`: total wall time only (the trace points synchronise the stream)
+    os.environ["QG_TRACE"] = "1"
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
