@@ -73,7 +73,7 @@ void init_pool() {
 void Workspace::release() {
   dev_free(u); dev_free(v); dev_free(h); dev_free(hb); dev_free(x);
   dev_free(dpu); dev_free(dpv); dev_free(tY); dev_free(tY2); dev_free(part);
-  dev_free(st); dev_free(d_nactive); dev_free(d_claim); dev_free(d_loop); dev_free(rk1);
+  dev_free(st); dev_free(d_nactive); dev_free(d_claim); dev_free(d_loop); dev_free(part2); dev_free(df); dev_free(rk1);
   h_nactive = nullptr;  // thread-local pinned word, owned by pinned_word()
 }
 
@@ -302,6 +302,30 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   W.d_claim = dev_alloc<int>(1);
   W.d_loop = dev_alloc<long long>(2);
   W.h_nactive = nullptr;
+  // deferred finalize (kFeatDF): one problem on the graph loop, no PSD blocks
+  // (their F' units run as a second kernel), no row partition; the unit rows
+  // are staged in shared memory (<= 2048 rows: 32 KB).  QG_DEFER_FIN=0: the
+  // finalize kernels of round 1 (A/B).
+  {
+    for (const Unit &u : H.xunits) H.max_unit_rows = std::max(H.max_unit_rows, u.row1 - u.row0);
+    for (const Unit &u : H.cones.units) H.max_unit_rows = std::max(H.max_unit_rows, u.row1 - u.row0);
+    // Default: problems whose operator step streams >= QG_DEFER_MIN_NNZ stored
+    // entries (P, A', A), where the SpMV hides the finalize (c3: 70.5 -> 47.6
+    // us per iteration; c2, 2.3e5 entries: 35.8 -> 37.2, so not there), and
+    // <= 4096 work units (CTA 0 sums 4 partials per unit: c5b's 5004 units
+    // measured neutral).  QG_DEFER_FIN=1 forces it on any eligible handle.
+    const char *e = std::getenv("QG_DEFER_FIN");
+    const char *emin = std::getenv("QG_DEFER_MIN_NNZ");
+    const int64_t min_nnz = emin ? std::atoll(emin) : 400000;
+    const bool want = e ? std::atoi(e) != 0 : (H.noffP[B] + 2 * H.noffA[B]) >= min_nnz;
+    H.defer_fin = want && B == 1 && !H.comm && !H.engine && H.cones.max_psd_order == 0 &&
+                  H.nxu() + H.nyu() > 0 && H.nxu() + H.nyu() <= 4096 && H.max_unit_rows <= 2048;
+    if (H.defer_fin) {
+      W.part2 = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
+      W.df = dev_alloc<DfCtl>(1);
+      QG_CUDA(cudaMemsetAsync(W.df, 0, sizeof(DfCtl), st));
+    }
+  }
   if (H.comm) {
     H.xred = dev_alloc<double>(H.NX);
     H.psum = dev_alloc<double>(2 * (size_t)B * kSlots);
@@ -339,6 +363,10 @@ static void launch_sub(const double *a, const double *b, double *out, int64_t n,
 }
 
 // ----------------------------------------------------------- LSMR loop --
+// Deferred finalize (kFeatDF launches) for this handle's loop steps: not
+// with the refine rank-one term (its steps use the all-features kernels).
+static bool defer_fin(const Handle &H) { return H.defer_fin && !H.use_rk1; }
+
 // Step / finalize arguments of one LSMR iteration (u-step with the deferred
 // update of the previous iteration, v-step), shared by the graph and the
 // persistent paths.
@@ -359,6 +387,20 @@ static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &
   fv.rk1 = rk1;
   // each follows a step kernel, which never writes the LSMR state or T entries
   fu.early = fv.early = 1;
+  if (defer_fin(H)) {
+    // each step's CTA 0 runs the finalize the previous step owes: the u-step
+    // finalizes the last v-step (partials in part2), the v-step the u-step
+    su.df = sv.df = W.df;
+    su.df_par = 0;
+    sv.df_par = 1;
+    sv.part = W.part2;
+    sv.fin = fu;
+    fin_ptrs(H, sv.fin);  // (reads part: the u-step's partials)
+    su.fin = fv;
+    fin_ptrs(H, su.fin);
+    su.fin.px = W.part2;
+    su.fin.py = W.part2 + (size_t)H.nxu() * kSlots;
+  }
 }
 
 static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStream_t st) {
@@ -370,11 +412,12 @@ static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStr
   StepArgs su, sv;
   FinArgs fu, fv;
   iter_args(H, jvp, su, sv, fu, fv);
+  const bool df = su.df != nullptr;  // finalizes run inside the next step (CTA 0)
   for (int i = 0; i < iters; ++i) {
     launch_step(H, M, ku, su, st);
-    launch_fin(H, M, fu, st);
+    if (!df) launch_fin(H, M, fu, st);
     launch_step(H, M, kv, sv, st);
-    launch_fin(H, M, fv, st);
+    if (!df) launch_fin(H, M, fv, st);
   }
 }
 
@@ -496,6 +539,7 @@ static int kernels_per_iter(const Handle &H) {
   // (+1: the F' step's PSD units as k_step_psd)
   const int psd = psd_split(H) ? 1 : 0;
   if (H.comm) return 8 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
+  if (defer_fin(H)) return 2;
   return 4 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
@@ -597,6 +641,12 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
     launch_engine(H, M, jvp, st);  // the whole loop, problem-resident (engine.cu)
   } else {
     run_lsmr_loop(H, M, jvp, cap, st);
+    if (defer_fin(H)) {  // the finalize the loop's last v-step still owes
+      StepArgs su, sv;
+      FinArgs fu, fv;
+      iter_args(H, jvp, su, sv, fu, fv);
+      launch_df_tail(H, M, fv, st);
+    }
     lsmr_flush(H, M, jvp, st);
   }
   QG_CUDA(cudaEventRecord(H.ev_loop[1], st));

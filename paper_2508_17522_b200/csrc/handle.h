@@ -55,6 +55,8 @@ struct SellMat {
   void release();
 };
 
+struct DfCtl;  // operator.h
+
 struct Workspace {
   double *u = nullptr, *v = nullptr, *h = nullptr, *hb = nullptr, *x = nullptr;  // EVec
   double *dpu = nullptr, *dpv = nullptr, *tY = nullptr, *tY2 = nullptr;          // Y
@@ -63,6 +65,8 @@ struct Workspace {
   Lsmr *st = nullptr;
   int *d_nactive = nullptr;
   int *d_claim = nullptr;    // problem claim counter of the resident engine
+  double *part2 = nullptr;   // v-step partial sums of deferred-finalize loops (u-steps use part)
+  DfCtl *df = nullptr;       // deferred-finalize control block (operator.h)
   long long *d_loop = nullptr;  // device-terminated graph loop: [iterations run, cap]
   int *h_nactive = nullptr;  // pinned
   void release();
@@ -96,6 +100,8 @@ struct Handle {
   int64_t *d_xunit_ptr = nullptr, *d_yunit_ptr = nullptr;
   int32_t *d_ft_order = nullptr;  // F' CTA -> unit order, PSD units first (null: natural order)
   int n_psd_units = 0;            // leading PSD units of d_ft_order (their own F' kernel, k_step_psd)
+  bool defer_fin = false;       // single-problem graph loop with the deferred finalize (kFeatDF)
+  int max_unit_rows = 0;         // rows of the longest work unit (kFeatDF staging)
   bool psd_split = true;         // QG_PSD_SPLIT at creation (0: PSD units stay in k_step, A/B)
   double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;
   double *Pxbar = nullptr;

@@ -214,8 +214,22 @@ constexpr int kStepThreads = 128;
 #ifndef QG_PSD_PREFETCH
 #define QG_PSD_PREFETCH 1
 #endif
-constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4;
+constexpr int kFeatDist = 1, kFeatRk1 = 2, kFeatWide = 4, kFeatDF = 8;
 constexpr int kFeatAll = kFeatDist | kFeatRk1 | kFeatWide;
+
+// Deferred finalize (kFeatDF, single-problem graph loops): CTA 0 of a step
+// launch runs the previous step's finalize and publishes its coefficients
+// (defined with the finalize kernels below).
+__device__ void df_fin(const Mats &M, const StepArgs &a);
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 // FEAT bits: kFeatWide (CTA-per-row units), kFeatDist (row-partitioned
 // X_PARTIAL / X_FINISH phases), kFeatRk1 (refine rank-one term, applied when
@@ -397,6 +411,150 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
     for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
 }
 
+// One work unit of a kFeatDF step (single problem, no PSD / row partition /
+// rank-one term): the SpMV row sums are staged in shared memory (2 doubles
+// per unit row) while CTA 0 finalizes the previous step; the row epilogues
+// then run from the staged sums with the published coefficients.  Same
+// per-row expressions as step_unit; the unit partials are summed over a
+// fixed row -> thread mapping.
+template <int KIND, int FEAT>
+__device__ __forceinline__ void step_unit_df(const Mats &M, const StepArgs &a, int ui) {
+  constexpr bool kWide = (FEAT & kFeatWide) != 0;
+  constexpr int kUnr = KIND == STEP_F ? QG_F_UNROLL : QG_FT_UNROLL;
+  constexpr int kRows32 = KIND == STEP_F ? QG_ROWS32 : QG_ROWS32_FT;
+  constexpr int kRowsG = KIND == STEP_F ? QG_ROWSG : QG_ROWSG_FT;
+  extern __shared__ double sm[];
+  __shared__ double red[kWarps * kSlots];
+  __shared__ DfPub sP;
+  const bool isx = ui < M.nxu;
+  const Unit u = isx ? M.xu[ui] : M.yu[ui - M.nxu];
+  const int p = u.prob;
+  const Embed E = M.emb[p];
+  pdl_wait();  // the previous step's vectors are complete past this point
+  const double *inX = a.in, *inY = a.in + M.NX;
+  double *stg = sm;  // staged row sums: [2 * (r - row0)] = s1, [+1] = s2
+  auto stage = [&](int r, double s1, double s2) {
+    stg[2 * (r - u.row0)] = s1;
+    stg[2 * (r - u.row0) + 1] = s2;
+  };
+  if (isx)
+    for_rows<kWide, kUnr, kRows32, kRowsG>(u, M.sP, &M.sAT, M.x_rowof, M.P_rp, M.P_col, M.P_val, M.AT_rp, M.AT_col,
+                                            M.AT_val, inX, KIND == STEP_F ? a.dpin : inY, u.lanes, M.xoff[p],
+                                            M.yoff[p], stage);
+  else
+    for_rows<kWide, kUnr, kRows32, kRowsG>(u, M.sA, nullptr, M.y_rowof, M.A_rp, M.A_col, M.A_val, nullptr, nullptr,
+                                            nullptr, inX, nullptr, u.lanes, M.xoff[p], 0, stage);
+  // the previous step's finalize (CTA 0 of this launch)
+  if (threadIdx.x == 0) {
+    const unsigned want = ld_acquire_u32(&a.df->flag[a.df_par ^ 1]) + 1;
+    while (ld_acquire_u32(&a.df->flag[a.df_par]) != want) __nanosleep(32);
+    const DfPub *g = &a.df->pub[a.df_par];
+    sP.s_in = __ldcg(&g->s_in); sP.c_out = __ldcg(&g->c_out); sP.wN = __ldcg(&g->wN);
+    sP.c_hbar = __ldcg(&g->c_hbar); sP.c_x = __ldcg(&g->c_x); sP.c_h = __ldcg(&g->c_h); sP.s_v = __ldcg(&g->s_v);
+    sP.runs = __ldcg(&g->runs); sP.upd = __ldcg(&g->upd);
+  }
+  __syncthreads();  // (also: every staged sum is in shared memory)
+  if (!sP.runs) return;  // CTA-uniform
+  const double wN = sP.wN, s_in = sP.s_in, c_out = sP.c_out;
+  double acc[kSlots] = {0.0, 0.0, 0.0, 0.0};
+  if (a.upd_h && sP.upd) {  // deferred vector update of the previous iteration (lsmr.py:142-144)
+    const double c1 = sP.c_hbar, c2 = sP.c_x, c3 = sP.c_h, sv = sP.s_v;
+    const int64_t off = isx ? 0 : M.NX;
+    for (int64_t r = off + u.row0 + threadIdx.x; r < off + u.row1; r += blockDim.x) {
+      const double hb = a.upd_h[r] - c1 * a.upd_hb[r];
+      const double x = a.upd_x[r] + c2 * hb;
+      a.upd_h[r] = a.in[r] * sv - c3 * a.upd_h[r];
+      a.upd_hb[r] = hb;
+      a.upd_x[r] = x;
+      acc[3] += x * x;
+    }
+  }
+  if (isx) {
+    for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+      const double s1 = stg[2 * (r - u.row0)], s2 = stg[2 * (r - u.row0) + 1];
+      const double w = inX[r];
+      double res;
+      if (KIND == STEP_F) {
+        const double o1 = (s1 + s2) + wN * M.q[r];
+        res = ((o1 - w) + w) / E.zN;
+        acc[0] += M.Pxbar[r] * w;
+      } else {
+        const double g = ((s1 - s2) - ((2.0 / E.tau) * wN) * M.Pxbar[r]) - wN * M.q[r];
+        res = ((g - w) + w) / E.zN;
+      }
+      acc[1] += M.q[r] * w;
+      const double o = s_in * res - (c_out != 0.0 ? c_out * a.old[r] : 0.0);
+      a.out[r] = o;
+      acc[2] += o * o;
+    }
+  } else {
+    double *outY = a.out + M.NX;
+    const double *oldY = a.old ? a.old + M.NX : nullptr;
+    if (KIND == STEP_F) {
+      for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+        const double o2 = (-stg[2 * (r - u.row0)]) + wN * M.b[r];
+        const double res = ((o2 - a.dpin[r]) + inY[r]) / E.zN;
+        const double o = s_in * res - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+        outY[r] = o;
+        acc[0] += M.b[r] * a.dpin[r];
+        acc[2] += o * o;
+      }
+    } else {
+      double *tY = a.tY;
+      for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x)
+        tY[r] = (stg[2 * (r - u.row0)] - wN * M.b[r]) - inY[r];
+      __syncthreads();
+      auto fin_row = [&](int r, double dpt) {
+        const double w = inY[r];
+        const double o = s_in * ((dpt + w) / E.zN) - (c_out != 0.0 ? c_out * oldY[r] : 0.0);
+        outY[r] = o;
+        acc[0] += M.b[r] * w;
+        acc[2] += o * o;
+        return o;
+      };
+      if (u.cls == CLS_ELEM) {
+        const int kind = M.dpi.blk[u.blk0].kind;
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) {
+          const double wgt = elem_weight(kind, M.dpi.dual, M.dpi.zmid[r]);
+          const double o = fin_row(r, wgt * tY[r]);
+          if (a.dpout) a.dpout[r] = wgt * o;
+        }
+      } else if (u.cls == CLS_TRI) {
+        for (int k = u.blk0 + (int)threadIdx.x; k < u.blk1; k += blockDim.x) {
+          const BlockInfo b = M.dpi.blk[k];
+          double D[9];
+#pragma unroll
+          for (int i = 0; i < 9; ++i) D[i] = M.dpi.tri_D[9 * b.param + i];
+          const int flip = M.dpi.tri_flip[b.param];
+          const double t3[3] = {tY[b.row], tY[b.row + 1], tY[b.row + 2]};
+          double r3[3], o3[3], d3[3];
+          tri_apply(D, flip, t3, r3);
+#pragma unroll
+          for (int i = 0; i < 3; ++i) o3[i] = fin_row(b.row + i, r3[i]);
+          if (a.dpout) {
+            tri_apply(D, flip, o3, d3);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) a.dpout[b.row + i] = d3[i];
+          }
+        }
+      } else if (u.cls == CLS_SOC && u.group > 0) {
+        soc_epilogue(M.dpi, u, tY, fin_row, outY, a.dpout);
+      } else {  // large SOC blocks: CTA-wide phases (no PSD in kFeatDF handles)
+        dpi_apply_unit(M.dpi, u, a.tY + u.row0, a.tY2 + u.row0, nullptr);
+        for (int r = u.row0 + threadIdx.x; r < u.row1; r += blockDim.x) fin_row(r, a.tY2[r]);
+        __syncthreads();
+        if (a.dpout) dpi_apply_unit(M.dpi, u, outY + u.row0, a.dpout + u.row0, nullptr);
+      }
+    }
+  }
+  pdl_trigger();
+  double tot[kSlots];
+  cta_sum_slots(acc, red, tot);
+  if (threadIdx.x == 0 && a.part)
+#pragma unroll
+    for (int k = 0; k < kSlots; ++k) a.part[(size_t)ui * kSlots + k] = tot[k];
+}
+
 // F' launches of batches with PSD blocks take their units in M.ft_order:
 // the PSD units (two D Pi applications of 4 dense products each: the
 // longest CTAs) first, so they start in the first wave instead of forming
@@ -404,6 +562,11 @@ __device__ __forceinline__ void step_unit(const Mats &M, const StepArgs &a, int 
 template <int KIND, int MINB, int FEAT>
 __global__ void __launch_bounds__(kStepThreads, MINB) k_step(Mats M, StepArgs a) {
   // (an X_FINISH launch covers only the X units: natural order)
+  if constexpr ((FEAT & kFeatDF) != 0) {  // CTA 0: the previous step's finalize; units from CTA 1
+    if (blockIdx.x == 0) df_fin(M, a);
+    else step_unit_df<KIND, FEAT>(M, a, (int)blockIdx.x - 1);
+    return;
+  }
   const int ui = (KIND == STEP_FT && M.ft_order && a.xmode != X_FINISH) ? M.ft_order[blockIdx.x] : (int)blockIdx.x;
   step_unit<KIND, FEAT, KIND == STEP_F && MINB == 8>(M, a, ui);
 }
@@ -632,26 +795,16 @@ __global__ void k_fin(Mats M, FinArgs a) {
 // slots, fixed-order CTA reduction, thread 0 runs the scalar part.  The
 // warp-per-problem version spent ~25 sequential L2 round trips per lane
 // summing c2's ~800 slots.
-__global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
-  const int p = (int)blockIdx.x;
-  // the LSMR state goes to shared memory in one coalesced sweep (the scalar
-  // recurrence then never waits on global memory for it), and back at the end
+// The per-problem finalize by one CTA (<= 256 threads), after its PDL wait:
+// fixed-order sums of the unit partials, thread 0 runs the scalar part on a
+// shared-memory copy of the LSMR state.  early: the state and T entries were
+// loaded before the wait (into sLw / *tv).
+__device__ __forceinline__ void fin_cta_run(const Mats &M, const FinArgs &a, int p, unsigned long long *sLw,
+                                            bool early, TVals *tv) {
   constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
-  static_assert(sizeof(Lsmr) % sizeof(unsigned long long) == 0, "Lsmr is copied as 8-byte words");
-  __shared__ unsigned long long sLw[kLw];
   Lsmr *Lsh = a.st ? reinterpret_cast<Lsmr *>(sLw) : nullptr;
   const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(a.st + p);
-  TVals tv{};
-  if (a.early) {
-    // loop finalizes (FinArgs::early): state and T entries issued ahead of
-    // the wait for the step kernel; L2 loads (cg): written by an earlier grid
-    if (Lsh)
-      for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = __ldcg(Lg + w);
-    if (threadIdx.x == 0) tv = load_tvals(M, a, p);
-  }
-  pdl_wait();
-  pdl_trigger();
-  if (!a.early && Lsh)
+  if (!early && Lsh)
     for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = Lg[w];
   if (fin_skips(a, p)) return;  // CTA-uniform
   __shared__ double red[(256 / 32) * 2 * kSlots];
@@ -679,13 +832,127 @@ __global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
       for (int w = 1; w < nw; ++w) t += red[w * 2 * kSlots + j];
       pre[j] = t;
     }
-    fin_problem(M, a, p, 0, pre, Lsh, a.early ? &tv : nullptr);
+    fin_problem(M, a, p, 0, pre, Lsh, early ? tv : nullptr);
   }
   if (Lsh) {
     __syncthreads();
     unsigned long long *Lw = reinterpret_cast<unsigned long long *>(a.st + p);
     for (int w = threadIdx.x; w < kLw; w += blockDim.x) Lw[w] = sLw[w];
   }
+}
+
+__global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
+  const int p = (int)blockIdx.x;
+  // the LSMR state goes to shared memory in one coalesced sweep (the scalar
+  // recurrence then never waits on global memory for it), and back at the end
+  constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
+  static_assert(sizeof(Lsmr) % sizeof(unsigned long long) == 0, "Lsmr is copied as 8-byte words");
+  __shared__ unsigned long long sLw[kLw];
+  const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(a.st + p);
+  TVals tv{};
+  if (a.early) {
+    // loop finalizes (FinArgs::early): state and T entries issued ahead of
+    // the wait for the step kernel; L2 loads (cg): written by an earlier grid
+    if (a.st)
+      for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = __ldcg(Lg + w);
+    if (threadIdx.x == 0) tv = load_tvals(M, a, p);
+  }
+  pdl_wait();
+  pdl_trigger();
+  fin_cta_run(M, a, p, sLw, a.early != 0, &tv);
+}
+
+// CTA 0 of a kFeatDF step launch (single problem): the finalize the previous
+// step owes (a.fin, its partials in the other part buffer), then the
+// coefficients of THIS step's row epilogues -> pub[par], released through
+// flag[par] = flag[par ^ 1] + 1 (the unit CTAs of this launch wait on it).
+// CTA 0 is the only reader / writer of the LSMR state and the T entries
+// during the launch.
+__device__ void df_fin(const Mats &M, const StepArgs &a) {
+  constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
+  __shared__ unsigned long long sLw[kLw];
+  __shared__ double red[kWarps * 2 * kSlots];
+  DfCtl *D = a.df;
+  const FinArgs &f = a.fin;
+  const int par = a.df_par, p = 0;
+  pdl_wait();
+  pdl_trigger();
+  // every load of the finalize at once (state, owed phase, T entries, unit
+  // partials): one L2 round trip before the scalar recurrence
+  const int pend = __ldcg(&D->pend_phase);
+  const unsigned long long *Lg = reinterpret_cast<const unsigned long long *>(f.st + p);
+  for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = __ldcg(Lg + w);
+  TVals tv{};
+  double wN0 = 0.0;
+  if (threadIdx.x == 0) {
+    tv = load_tvals(M, f, p);
+    wN0 = __ldcg(a.in + M.NX + M.NY + p);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+  double s[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (pend) {
+#pragma unroll 8
+    for (int64_t k = f.px_ptr[p] + threadIdx.x; k < f.px_ptr[p + 1]; k += blockDim.x)
+#pragma unroll
+      for (int j = 0; j < kSlots; ++j) s[j] += __ldcg(f.px + k * kSlots + j);
+#pragma unroll 8
+    for (int64_t k = f.py_ptr[p] + threadIdx.x; k < f.py_ptr[p + 1]; k += blockDim.x)
+#pragma unroll
+      for (int j = 0; j < kSlots; ++j) s[kSlots + j] += __ldcg(f.py + k * kSlots + j);
+  }
+#pragma unroll
+  for (int j = 0; j < 2 * kSlots; ++j) s[j] = warp_sum(s[j]);
+  if (lane == 0)
+#pragma unroll
+    for (int j = 0; j < 2 * kSlots; ++j) red[warp * 2 * kSlots + j] = s[j];
+  __syncthreads();
+  Lsmr *L = reinterpret_cast<Lsmr *>(sLw);
+  if (threadIdx.x == 0) {
+    double wN = wN0;
+    // the owed finalize (fin_problem's work on the shared copy; an inactive
+    // problem has nothing to finalize, as fin_skips)
+    if (pend && L->active) {
+      double pre[2 * kSlots];
+#pragma unroll
+      for (int j = 0; j < 2 * kSlots; ++j) {
+        double t = red[j];
+        for (int w = 1; w < nw; ++w) t += red[w * 2 * kSlots + j];
+        pre[j] = t;
+      }
+      const int64_t T = M.NX + M.NY + p;
+      const int w = fin_core(M.emb[p], f.phase, f.kind, L, pre, pre + kSlots, tv, false, true);
+      if (w & TV_OUT) { f.out[T] = tv.out; wN = tv.out; }  // (f.out is this step's input)
+      if (w & TV_H) f.h[T] = tv.h;
+      if (w & TV_HB) f.hb[T] = tv.hb;
+      if (w & TV_X) f.x[T] = tv.x;
+    }
+    DfPub P;
+    P.runs = (L->active && !(a.is_v_step && L->skip_v)) ? 1 : 0;
+    P.s_in = L->s_in;
+    P.c_out = L->c_out;
+    P.wN = wN;
+    P.upd = L->itn > 0 ? 1 : 0;
+    P.c_hbar = L->c_hbar; P.c_x = L->c_x; P.c_h = L->c_h; P.s_v = L->s_v;
+    D->pub[par] = P;
+    D->pend_phase = a.is_v_step ? PH_STEP_V : PH_STEP_U;  // this step's finalize is owed to the next
+    __threadfence();
+    st_release_u32(&D->flag[par], __ldcg(&D->flag[par ^ 1]) + 1);
+  }
+  __syncthreads();
+  if (pend) {  // the finalized state back to global memory (read by the next step's CTA 0)
+    unsigned long long *Lw = reinterpret_cast<unsigned long long *>(f.st + p);
+    for (int w = threadIdx.x; w < kLw; w += blockDim.x) Lw[w] = sLw[w];
+  }
+}
+
+// The finalize the last step of a kFeatDF loop owes (after the loop).
+__global__ void __launch_bounds__(256) k_df_tail(Mats M, FinArgs a, DfCtl *D) {
+  constexpr int kLw = (int)(sizeof(Lsmr) / sizeof(unsigned long long));
+  __shared__ unsigned long long sLw[kLw];
+  if (__ldcg(&D->pend_phase) != a.phase) return;  // (no iteration ran: nothing owed)
+  fin_cta_run(M, a, 0, sLw, false, nullptr);
+  __syncthreads();
+  if (threadIdx.x == 0) D->pend_phase = 0;
 }
 
 // (Measured and dropped: the same loop as ONE 1024-thread CTA for a single
@@ -734,11 +1001,15 @@ void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long c
 // opt == 0 the reference default 20 (n + m + 1) (lsmr.py:69-70 on the
 // embedding).  Thread 0 also arms the device-terminated loop: [0, cap].
 __global__ void k_init_state(Lsmr *st, int B, double atol, double btol, long long opt, const int64_t *xoff,
-                             const int64_t *yoff, long long *loop, long long cap) {
+                             const int64_t *yoff, long long *loop, long long cap, DfCtl *df) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p == 0 && loop) {
     loop[0] = 0;
     loop[1] = cap;
+  }
+  if (p == 0 && df) {  // deferred-finalize loops start with nothing owed, publication counters at 0
+    df->flag[0] = df->flag[1] = 0;
+    df->pend_phase = 0;
   }
   if (p >= B) return;
   Lsmr L{};
@@ -865,6 +1136,7 @@ static size_t psd_step_smem(const Handle &H) {
 // k_step over `grid` units (the unit order of M), on st with PDL.
 static void launch_step_main(const Handle &H, const Mats &M, int kind, const StepArgs &a, unsigned grid,
                              size_t smem, cudaStream_t st) {
+  // (grid is captured by reference in `go`: kFeatDF launches add CTA 0)
   static int threads = 0;
   if (!threads) {  // QG_STEP_THREADS: A/B switch for the CTA size (32..128)
     const char *e = std::getenv("QG_STEP_THREADS");
@@ -884,6 +1156,19 @@ static void launch_step_main(const Handle &H, const Mats &M, int kind, const Ste
     launch_pdl(kern, dim3(grid), dim3(threads), sm_bytes, st, M, a);
   };
   const int feat = step_feat(H, a);
+  if (a.df) {  // deferred finalize: CTA 0 + the units, row sums staged in shared memory
+    grid += 1;
+    const size_t stg = (size_t)2 * H.max_unit_rows * sizeof(double);
+    if (kind == STEP_F) {
+      if (feat & kFeatWide) go(k_step<STEP_F, 12, kFeatWide | kFeatDF>, stg);
+      else go(k_step<STEP_F, 12, kFeatDF>, stg);
+    } else {
+      if (feat & kFeatWide) go(k_step<STEP_FT, 12, kFeatWide | kFeatDF>, stg);
+      else go(k_step<STEP_FT, 12, kFeatDF>, stg);
+    }
+    QG_LAUNCHED();
+    return;
+  }
   if (kind == STEP_F) {
     if (feat == kFeatAll) go(k_step<STEP_F, 12, kFeatAll>, 0);
     else if (feat == kFeatWide) go(k_step<STEP_F, 12, kFeatWide>, 0);
@@ -972,8 +1257,19 @@ void launch_count_active(const Handle &H, cudaStream_t st) {
   QG_LAUNCHED();
 }
 
+void launch_df_tail(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
+  FinArgs a = a0;
+  a.px = H.ws.part2;  // the v-step's partials
+  a.px_ptr = H.d_xunit_ptr;
+  a.py = H.ws.part2 + (size_t)H.nxu() * kSlots;
+  a.py_ptr = H.d_yunit_ptr;
+  k_df_tail<<<1, 256, 0, st>>>(M, a, H.ws.df);
+  QG_LAUNCHED();
+}
+
 void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st) {
-  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, opt, H.d_xoff, H.d_yoff, H.ws.d_loop, cap);
+  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, opt, H.d_xoff, H.d_yoff, H.ws.d_loop, cap,
+                                                  H.ws.df);
   QG_LAUNCHED();
 }
 

@@ -31,6 +31,22 @@ struct FinArgs {
   int early = 0;
 };
 
+// Deferred finalize of single-problem graph loops (kFeatDF steps): CTA 0
+// of every step launch runs the PREVIOUS step's finalize and publishes the
+// coefficients this step's row epilogues need; the other CTAs stage their
+// row sums in shared memory meanwhile and wait for pub[par] (flag[par] ==
+// flag[par ^ 1] + 1).  pend_phase: the finalize still owed by the last step
+// (0: none).
+struct DfPub {
+  double s_in, c_out, wN, c_hbar, c_x, c_h, s_v;
+  int runs, upd;
+};
+struct DfCtl {
+  DfPub pub[2];
+  unsigned flag[2];
+  int pend_phase, pad;
+};
+
 struct StepArgs {
   const double *in;    // EVec, raw
   const double *dpin;  // Y: D Pi applied to in_Y (F step)
@@ -52,6 +68,10 @@ struct StepArgs {
   // F step out -= r w_N ; F' step T out -= r'w (dot partial in slot 3)
   const double *rk1 = nullptr;
   unsigned long long *prof = nullptr;  // QG_PSD_PROF diagnostics (qg_time_kernel): PSD unit phase cycles
+  // deferred finalize (kFeatDF launches: CTA 0 finalizes, units from blockIdx 1)
+  DfCtl *df = nullptr;
+  int df_par = 0;   // this step's publication slot (u-step 0, v-step 1)
+  FinArgs fin{};    // the previous step's finalize (its partial sums in the other part buffer)
 };
 
 struct UpdArgs {
@@ -70,6 +90,7 @@ void fin_ptrs(const Handle &H, FinArgs &a);  // partial-sum producers of a whole
 void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_t st);
 void launch_count_active(const Handle &H, cudaStream_t st);
 void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st);
+void launch_df_tail(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);  // owed finalize after the loop
 void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st);
 void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long chunk, cudaStream_t st);
 
