@@ -146,6 +146,21 @@ struct Tracer {
   void operator()(const char *what) { trace_point(what, st); }
 };
 
+// The deferred-finalize loop (kFeatDF) is wanted for one problem, no PSD
+// blocks (their F' units run as a second kernel), no row partition, whose
+// operator step streams >= 1e5 stored entries (P, A', A): there the SpMV
+// hides CTA 0's finalize (c3: 70.5 -> 47.6 us per LSMR iteration; c2 with
+// 1024-entry units: 35.3 -> 30.0).  QG_DEFER_FIN=0|1 forces it off / on
+// (where eligible).
+static bool defer_fin_intent(const Handle &H, const qg_batch_desc &d) {
+  if (H.B != 1 || H.comm) return false;
+  for (int64_t i = 0; i < d.nblocks[0]; ++i)
+    if (d.blocks[i].kind == QG_CONE_PSD) return false;
+  const char *e = std::getenv("QG_DEFER_FIN");
+  if (e) return std::atoi(e) != 0;
+  return H.noffP[1] + 2 * H.noffA[1] >= 100000;
+}
+
 static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   NvtxRange nv("qg:prepare");
   Tracer trace(st);
@@ -190,7 +205,15 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   const int64_t total = nnzX + nnzY + H.NX + H.NY;
   // small problems get small units (all SMs busy, short per-warp chains),
   // large batches amortise per-CTA work over up to 16k entries
-  int64_t target_nnz = std::max<int64_t>(256, std::min<int64_t>(16384, total / (8 * 148) + 1));
+  // (a single problem caps units at 8k entries: c5b's dense LASSO rows run
+  // 542 -> 502 us per LSMR iteration with 4k..10k-entry units vs 16k)
+  const int64_t cap_nnz = B == 1 ? 8192 : 16384;
+  int64_t target_nnz = std::max<int64_t>(256, std::min<int64_t>(cap_nnz, total / (8 * 148) + 1));
+  // a single problem on the deferred-finalize loop (below): CTA 0 sums 4
+  // partials per unit, so units of >= 1024 entries (c2: 914 -> ~230 units,
+  // 35.3 -> 30.0 us per LSMR iteration)
+  const bool df_intent = defer_fin_intent(H, d);
+  if (df_intent) target_nnz = std::max<int64_t>(target_nnz, 1024);
   if (const char *e = std::getenv("QG_TARGET_NNZ")) target_nnz = std::max<int64_t>(64, std::atoll(e));  // A/B
   const double avg_y = H.NY ? (double)nnzY / H.NY + 1.0 : 1.0;
   const int64_t target_rows_y = std::max<int64_t>(8, std::min<int64_t>(4096, (int64_t)(target_nnz / avg_y)));
@@ -309,17 +332,10 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
   {
     for (const Unit &u : H.xunits) H.max_unit_rows = std::max(H.max_unit_rows, u.row1 - u.row0);
     for (const Unit &u : H.cones.units) H.max_unit_rows = std::max(H.max_unit_rows, u.row1 - u.row0);
-    // Default: problems whose operator step streams >= QG_DEFER_MIN_NNZ stored
-    // entries (P, A', A), where the SpMV hides the finalize (c3: 70.5 -> 47.6
-    // us per iteration; c2, 2.3e5 entries: 35.8 -> 37.2, so not there), and
-    // <= 4096 work units (CTA 0 sums 4 partials per unit: c5b's 5004 units
-    // measured neutral).  QG_DEFER_FIN=1 forces it on any eligible handle.
-    const char *e = std::getenv("QG_DEFER_FIN");
-    const char *emin = std::getenv("QG_DEFER_MIN_NNZ");
-    const int64_t min_nnz = emin ? std::atoll(emin) : 400000;
-    const bool want = e ? std::atoi(e) != 0 : (H.noffP[B] + 2 * H.noffA[B]) >= min_nnz;
-    H.defer_fin = want && B == 1 && !H.comm && !H.engine && H.cones.max_psd_order == 0 &&
-                  H.nxu() + H.nyu() > 0 && H.nxu() + H.nyu() <= 4096 && H.max_unit_rows <= 2048;
+    // <= 4096 work units: CTA 0 sums 4 partials per unit (c5b's 5004+ units:
+    // neutral)
+    H.defer_fin = defer_fin_intent(H, d) && !H.engine && H.nxu() + H.nyu() > 0 && H.nxu() + H.nyu() <= 4096 &&
+                  H.max_unit_rows <= 2048;
     if (H.defer_fin) {
       W.part2 = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
       W.df = dev_alloc<DfCtl>(1);
