@@ -280,12 +280,18 @@ __device__ __forceinline__ void region_dot2(const EngView &V, int r, bool ra, in
 }
 
 // Phase A: the row sums of one operator application into rs (X rows: P w1
-// +- A' (D Pi) w2 ; Y rows: A w1).  Warp w takes slices w, w + nw, ...,
-// two per round when both are on the same side (their loads overlap).
+// +- A' (D Pi) w2 ; Y rows: A w1).  Slot i takes slices i, i + nw, ...,
+// two per round when both are on the same side (their loads overlap), so
+// the last slots hold the fewest slices.  While warp 0 runs the scalar
+// finalize (fin_warp) it takes the LAST slot and warp w slot w - 1: warp 0
+// was the phase's critical path (c5a: finalize 5k + a full slice share 14k
+// cycles of a 19.5k-cycle A_u).  Each row is summed by one lane in storage
+// order whichever warp owns it, so the sums do not depend on the mapping.
 template <int KIND>
 __device__ __forceinline__ void eng_spmv(const EngView &V, int n, int m, const double *in, const double *dp,
-                                         double *rs) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
+                                         double *rs, bool fin_warp) {
+  const int lane = threadIdx.x & 31, nw = (int)(blockDim.x >> 5);
+  const int warp = fin_warp ? (int)((threadIdx.x >> 5) + nw - 1) % nw : (int)(threadIdx.x >> 5);
   const int nxs = V.hd()->nxs, ntot = nxs + V.hd()->nys;
   const double *x2 = KIND == STEP_F ? dp : in + n;  // A' gathers D Pi w_2 (F) or w_2 (F')
   for (int qa0 = warp; qa0 < ntot; qa0 += 2 * nw) {
@@ -664,7 +670,7 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
           }
           __syncwarp();
         }
-        eng_spmv<KU>(V, n, m, sv, dp, rs);
+        eng_spmv<KU>(V, n, m, sv, dp, rs, pending_v);
         if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
         tick(1);
@@ -691,7 +697,7 @@ __global__ void __launch_bounds__(NT, MINB) k_engine(Mats M, EngArgs a) {
           }
           __syncwarp();
         }
-        eng_spmv<KV>(V, n, m, su, dp, rs);
+        eng_spmv<KV>(V, n, m, su, dp, rs, true);
         if (prof1) S.prof[7] += (unsigned long long)(clock64() - t_sp);
         __syncthreads();
         tick(3);
