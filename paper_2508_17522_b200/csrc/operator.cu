@@ -59,6 +59,22 @@ __device__ __forceinline__ bool lsmr_runs(const StepArgs &a, int p, double &s_in
 #ifndef QG_SLICE_CLAIM
 #define QG_SLICE_CLAIM 2  // SELL slices claimed (and streamed together) per warp: 1 or 2
 #endif
+// One row sum kept by a lane until its epilogue runs (for_rows' CSR paths).
+struct RowKeep {
+  double s1 = 0.0, s2 = 0.0;
+  int r = -1;
+  __device__ __forceinline__ void set(int row, double a, double b) {
+    r = row;
+    s1 = a;
+    s2 = b;
+  }
+  template <class RowFn>
+  __device__ __forceinline__ void flush(RowFn &row) {
+    if (r >= 0) row(r, s1, s2);
+    r = -1;
+  }
+};
+
 template <bool WIDE, int UNR, int ROWS32, int ROWSG, class RowFn>
 __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, const SellView *S2,
                                          const int32_t *rowof, const int32_t *rp1, const int32_t *c1,
@@ -108,10 +124,24 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
     }
   } else if (G == 32) {
     // warp per row with a compile-time lane stride: the loop unrolls into
-    // independent loads (a runtime stride measured 7x slower on C5b)
+    // independent loads (a runtime stride measured 7x slower on C5b).
+    // Row epilogues are spread over the lanes: after the xor reduction every
+    // lane holds the row's sums, lane k keeps the warp's k-th row (mod 32)
+    // and every 32 rows (and at the end) each lane runs row() for the row it
+    // keeps -- 32 epilogues (their loads) in parallel instead of lane 0
+    // running them one after another
+    RowKeep keep;
+    int k = 0;
+    auto put = [&](int r, double a, double b) {
+      if (lane == k) keep.set(r, a, b);
+      if (++k == 32) {
+        keep.flush(row);
+        k = 0;
+      }
+    };
     if constexpr (ROWS32 > 1) {
       // ROWS32 rows of the warp's row sequence at once (same rows, same
-      // order of row() calls as the one-row loop)
+      // order as the one-row loop)
       const int nw = (int)(blockDim.x >> 5);
       constexpr int R = ROWS32;
       for (int r0 = u.row0 + warp; r0 < u.row1; r0 += R * nw) {
@@ -123,10 +153,9 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
           s1[j] = warp_sum(s1[j]);
           s2[j] = rp2 ? warp_sum(s2[j]) : 0.0;
         }
-        if (lane == 0)
 #pragma unroll
-          for (int j = 0; j < R; ++j)
-            if (r0 + j * nw < u.row1) row(r0 + j * nw, s1[j], s2[j]);
+        for (int j = 0; j < R; ++j)
+          if (r0 + j * nw < u.row1) put(r0 + j * nw, s1[j], s2[j]);
       }
     } else {
       for (int r = u.row0 + warp; r < u.row1; r += (int)(blockDim.x >> 5)) {
@@ -134,16 +163,27 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
         double s2 = rp2 ? row_dot32(rp2, c2, v2, x2, r, lane) : 0.0;
         s1 = warp_sum(s1);
         s2 = warp_sum(s2);
-        if (lane == 0) row(r, s1, s2);
+        put(r, s1, s2);
       }
     }
+    keep.flush(row);
   } else {
     // G lanes per CSR row (G from the average row length of the matrices),
-    // loops warp-uniform so every lane reaches the shuffles
+    // loops warp-uniform so every lane reaches the shuffles; the epilogues
+    // are spread over each group's G lanes as above (lane lg keeps the
+    // group's k-th row mod G)
     const int lg = lane & (G - 1), gpw = 32 / G, nw = (int)(blockDim.x >> 5);
+    RowKeep keep;
+    int k = 0;
+    auto put = [&](bool valid, int r, double a, double b) {
+      if (valid && lg == k) keep.set(r, a, b);
+      if (++k == G) {
+        keep.flush(row);
+        k = 0;
+      }
+    };
     if constexpr (ROWSG > 1) {
-      // ROWSG row groups of the warp's sequence at once; each lane still
-      // calls row() for its rows in the one-group order
+      // ROWSG row groups of the warp's sequence at once
       constexpr int R = ROWSG;
       const int stride = nw * gpw;
       for (int base = u.row0 + warp * gpw; base < u.row1; base += R * stride) {
@@ -156,10 +196,8 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
           s1[j] = gsum(s1[j], G);
           s2[j] = rp2 ? gsum(s2[j], G) : 0.0;
         }
-        if (lg == 0)
 #pragma unroll
-          for (int j = 0; j < R; ++j)
-            if (r + j * stride < u.row1) row(r + j * stride, s1[j], s2[j]);
+        for (int j = 0; j < R; ++j) put(r + j * stride < u.row1, r + j * stride, s1[j], s2[j]);
       }
     } else {
       for (int base = u.row0 + warp * gpw; base < u.row1; base += nw * gpw) {
@@ -169,9 +207,10 @@ __device__ __forceinline__ void for_rows(const Unit &u, const SellView &S1, cons
         double s2 = (valid && rp2) ? row_dot(rp2, c2, v2, x2, r, lg, G) : 0.0;
         s1 = gsum(s1, G);
         s2 = gsum(s2, G);
-        if (valid && lg == 0) row(r, s1, s2);
+        put(valid, r, s1, s2);
       }
     }
+    keep.flush(row);
   }
 }
 
