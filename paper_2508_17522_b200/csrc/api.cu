@@ -334,8 +334,9 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     for (const Unit &u : H.cones.units) H.max_unit_rows = std::max(H.max_unit_rows, u.row1 - u.row0);
     // <= 4096 work units: CTA 0 sums 4 partials per unit (c5b's 5004+ units:
     // neutral)
-    H.defer_fin = defer_fin_intent(H, d) && !H.engine && H.nxu() + H.nyu() > 0 && H.nxu() + H.nyu() <= 4096 &&
-                  H.max_unit_rows <= 2048;
+    // (no CTA-per-row units: that path is not exercised by any eligible config)
+    H.defer_fin = defer_fin_intent(H, d) && !H.engine && !H.has_wide && H.nxu() + H.nyu() > 0 &&
+                  H.nxu() + H.nyu() <= 4096 && H.max_unit_rows <= 2048;
     if (H.defer_fin) {
       W.part2 = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
       W.df = dev_alloc<DfCtl>(1);

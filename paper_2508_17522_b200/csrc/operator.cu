@@ -1200,13 +1200,9 @@ static void launch_step_main(const Handle &H, const Mats &M, int kind, const Ste
   if (a.df) {  // deferred finalize: CTA 0 + the units, row sums staged in shared memory
     grid += 1;
     const size_t stg = (size_t)2 * H.max_unit_rows * sizeof(double);
-    if (kind == STEP_F) {
-      if (feat & kFeatWide) go(k_step<STEP_F, 12, kFeatWide | kFeatDF>, stg);
-      else go(k_step<STEP_F, 12, kFeatDF>, stg);
-    } else {
-      if (feat & kFeatWide) go(k_step<STEP_FT, 12, kFeatWide | kFeatDF>, stg);
-      else go(k_step<STEP_FT, 12, kFeatDF>, stg);
-    }
+    (void)feat;  // (deferred-finalize handles have no CTA-per-row units: api.cu)
+    if (kind == STEP_F) go(k_step<STEP_F, 12, kFeatDF>, stg);
+    else go(k_step<STEP_FT, 12, kFeatDF>, stg);
     QG_LAUNCHED();
     return;
   }
