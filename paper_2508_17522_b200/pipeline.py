@@ -3,8 +3,9 @@
 ``evaluate_host`` is the end-to-end entry for a batch that lives in (pinned)
 host memory: problem data, solutions and directions in, jvp and vjp outputs
 out.  The batch is cut into ``chunks`` contiguous problem ranges; chunk k+1's
-host-to-device copies and chunk k-1's device-to-host copies run on a copy
-stream while chunk k's preparation + jvp + vjp run on the compute stream, so
+host-to-device copies and chunk k-1's device-to-host copies run on two copy
+streams (one per copy engine) while chunk k's preparation + jvp + vjp run on
+the compute stream, so
 PCIe time hides behind the kernels instead of adding to them.
 
 Problems are independent, so per-problem results equal a whole-batch call up
@@ -78,7 +79,8 @@ def evaluate_host(n, m, P_nnz, A_nnz, blocks, data, dirs, *, chunks=4, atol=1e-1
     if out is None:
         out = {k: torch.empty(int(v), dtype=torch.float64, pin_memory=True) for k, v in shapes.items()}
     comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream()
+    copy = torch.cuda.Stream()   # host -> device
+    down = torch.cuda.Stream()   # device -> host (the other copy engine: runs beside the uploads)
     bounds = chunk_bounds(B, chunks)
     f64, i64 = torch.float64, torch.int64
     kw = dict(atol=atol, btol=btol, max_iter=max_iter)
@@ -123,13 +125,14 @@ def evaluate_host(n, m, P_nnz, A_nnz, blocks, data, dirs, *, chunks=4, atol=1e-1
         r = _ranges(o, lo, hi)
         res = dict(dx=(dx, "dx"), dy=(dy, "dy"), ds=(ds, "ds"), gP=(gP, "dP"), gA=(gA, "dA"), gq=(gq, "dq"),
                    gb=(gb, "db"))
-        copy.wait_stream(comp)
-        with torch.cuda.stream(copy):
+        down.wait_stream(comp)
+        with torch.cuda.stream(down):
             for k, (v, rk) in res.items():
                 a, e = (int(x) for x in r[rk])
                 out[k][a:e].copy_(v[:e - a], non_blocking=True)
         keep.append((t, res))
     copy.synchronize()
+    down.synchronize()
     comp.synchronize()
     del keep
     return out, diags_j, diags_v
