@@ -1164,6 +1164,14 @@ struct SideStream {
     QG_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     QG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
   }
+  ~SideStream() {  // at host-thread exit (errors ignored: the context may be gone at process exit)
+    if (join) cudaEventDestroy(join);
+    if (fork) cudaEventDestroy(fork);
+    if (s) cudaStreamDestroy(s);
+    cudaGetLastError();
+  }
+  SideStream(const SideStream &) = delete;
+  SideStream &operator=(const SideStream &) = delete;
 };
 
 bool psd_split(const Handle &H) { return H.psd_split && H.n_psd_units > 0; }
