@@ -146,16 +146,14 @@ struct Tracer {
   void operator()(const char *what) { trace_point(what, st); }
 };
 
-// The deferred-finalize loop (kFeatDF) is wanted for one problem, no PSD
-// blocks (their F' units run as a second kernel), no row partition, whose
+// The deferred-finalize loop (kFeatDF) is wanted for one problem, no row
+// partition, whose
 // operator step streams >= 1e5 stored entries (P, A', A): there the SpMV
 // hides CTA 0's finalize (c3: 70.5 -> 47.6 us per LSMR iteration; c2 with
 // 1024-entry units: 35.3 -> 30.0).  QG_DEFER_FIN=0|1 forces it off / on
 // (where eligible).
 static bool defer_fin_intent(const Handle &H, const qg_batch_desc &d) {
   if (H.B != 1 || H.comm) return false;
-  for (int64_t i = 0; i < d.nblocks[0]; ++i)
-    if (d.blocks[i].kind == QG_CONE_PSD) return false;
   const char *e = std::getenv("QG_DEFER_FIN");
   if (e) return std::atoi(e) != 0;
   return H.noffP[1] + 2 * H.noffA[1] >= 100000;
@@ -335,8 +333,13 @@ static void build_handle(Handle &H, const qg_batch_desc &d, cudaStream_t st) {
     // <= 4096 work units: CTA 0 sums 4 partials per unit (c5b's 5004+ units:
     // neutral)
     // (no CTA-per-row units: that path is not exercised by any eligible config)
+    // PSD blocks: only with their F' units in k_step_psd, and then only the F
+    // step defers (mixed loop: the F' step is the split launch, its finalize
+    // runs in the next F step's CTA 0, the F step's own in a k_fin_cta)
+    const bool psd = H.cones.max_psd_order > 0;
     H.defer_fin = defer_fin_intent(H, d) && !H.engine && !H.has_wide && H.nxu() + H.nyu() > 0 &&
-                  H.nxu() + H.nyu() <= 4096 && H.max_unit_rows <= 2048;
+                  H.nxu() + H.nyu() <= 4096 && H.max_unit_rows <= 2048 && (!psd || psd_split(H));
+    H.df_mixed = H.defer_fin && psd;
     if (H.defer_fin) {
       W.part2 = dev_alloc<double>((size_t)(H.nxu() + H.nyu() + 1) * kSlots);
       W.df = dev_alloc<DfCtl>(1);
@@ -382,7 +385,13 @@ static void launch_sub(const double *a, const double *b, double *out, int64_t n,
 // ----------------------------------------------------------- LSMR loop --
 // Deferred finalize (kFeatDF launches) for this handle's loop steps: not
 // with the refine rank-one term (its steps use the all-features kernels).
-static bool defer_fin(const Handle &H) { return H.defer_fin && !H.use_rk1; }
+static bool host_loop() {  // QG_HOST_LOOP=1: the host-polled chunk loop (chunks of 1..64 iterations)
+  static const char *env = std::getenv("QG_HOST_LOOP");
+  return env && std::atoi(env) != 0;
+}
+// (not on the host-polled loop: its odd chunk lengths would break the mixed
+// loop's alternating publication slots)
+static bool defer_fin(const Handle &H) { return H.defer_fin && !H.use_rk1 && !host_loop(); }
 
 // Step / finalize arguments of one LSMR iteration (u-step with the deferred
 // update of the previous iteration, v-step), shared by the graph and the
@@ -404,19 +413,32 @@ static void iter_args(Handle &H, bool jvp, StepArgs &su, StepArgs &sv, FinArgs &
   fv.rk1 = rk1;
   // each follows a step kernel, which never writes the LSMR state or T entries
   fu.early = fv.early = 1;
-  if (defer_fin(H)) {
+  if (defer_fin(H) && !H.df_mixed) {
     // each step's CTA 0 runs the finalize the previous step owes: the u-step
     // finalizes the last v-step (partials in part2), the v-step the u-step
     su.df = sv.df = W.df;
     su.df_par = 0;
     sv.df_par = 1;
+    su.df_next = PH_STEP_U;
+    sv.df_next = PH_STEP_V;
     sv.part = W.part2;
     sv.fin = fu;
     fin_ptrs(H, sv.fin);  // (reads part: the u-step's partials)
     su.fin = fv;
+    su.fin.part = W.part2;
     fin_ptrs(H, su.fin);
-    su.fin.px = W.part2;
-    su.fin.py = W.part2 + (size_t)H.nxu() * kSlots;
+  } else if (defer_fin(H)) {
+    // mixed (PSD blocks): the F step's CTA 0 runs the finalize of the F' step
+    // before it (partials in part); the F step writes part2, finalized by a
+    // k_fin_cta after it.  df_par alternates per iteration (capture_iters).
+    StepArgs &sF = jvp ? su : sv;
+    FinArgs &fFT = jvp ? fv : fu, &fF = jvp ? fu : fv;
+    sF.df = W.df;
+    sF.df_next = fFT.phase;
+    sF.part = W.part2;
+    sF.fin = fFT;
+    fin_ptrs(H, sF.fin);
+    fF.part = W.part2;
   }
 }
 
@@ -429,12 +451,14 @@ static void capture_iters(Handle &H, const Mats &M, bool jvp, int iters, cudaStr
   StepArgs su, sv;
   FinArgs fu, fv;
   iter_args(H, jvp, su, sv, fu, fv);
-  const bool df = su.df != nullptr;  // finalizes run inside the next step (CTA 0)
+  const bool df = su.df != nullptr && sv.df != nullptr;  // finalizes run inside the next step (CTA 0)
+  const bool mixed = !df && (su.df != nullptr || sv.df != nullptr);  // only the F step defers
   for (int i = 0; i < iters; ++i) {
+    if (mixed) (jvp ? su : sv).df_par = i & 1;  // successive F steps alternate slots (chunks are even)
     launch_step(H, M, ku, su, st);
-    if (!df) launch_fin(H, M, fu, st);
+    if (!df && !(mixed && !jvp)) launch_fin(H, M, fu, st);  // (vjp: fin U runs in the F step's CTA 0)
     launch_step(H, M, kv, sv, st);
-    if (!df) launch_fin(H, M, fv, st);
+    if (!df && !(mixed && jvp)) launch_fin(H, M, fv, st);   // (jvp: fin V runs in the next F step's CTA 0)
   }
 }
 
@@ -556,14 +580,16 @@ static int kernels_per_iter(const Handle &H) {
   // (+1: the F' step's PSD units as k_step_psd)
   const int psd = psd_split(H) ? 1 : 0;
   if (H.comm) return 8 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0) - (H.nxu() == 0 ? 2 : 0);
-  if (defer_fin(H)) return 2;
+  if (defer_fin(H)) return H.df_mixed ? 3 + psd : 2;
   return 4 + psd - (H.nxu() + H.nyu() == 0 ? 2 : 0);
 }
 
 static void run_lsmr_loop(Handle &H, const Mats &M, bool jvp, long long cap, cudaStream_t st) {
   Workspace &W = H.ws;
-  const char *env = std::getenv("QG_HOST_LOOP");  // A/B: the host-polled chunk loop
-  if ((!H.comm || H.comm->capturable()) && !(env && std::atoi(env) != 0)) {
+  // deferred finalize: nothing owed at the start, except in a mixed vjp loop,
+  // whose first F' step's finalize runs in the first F step
+  if (defer_fin(H)) launch_init_df(H, H.df_mixed && !jvp ? PH_STEP_U : 0, st);
+  if ((!H.comm || H.comm->capturable()) && !host_loop()) {
     // W.d_loop = [0, cap] was armed by k_init_state
     if (cap > 0) launch_iters(H, M, jvp, -kWhileChunk, st);
     H.while_pending = true;
@@ -658,10 +684,14 @@ static void lsmr_solve(Handle &H, const Mats &M, bool jvp, int rhs_kind, long lo
     launch_engine(H, M, jvp, st);  // the whole loop, problem-resident (engine.cu)
   } else {
     run_lsmr_loop(H, M, jvp, cap, st);
-    if (defer_fin(H)) {  // the finalize the loop's last v-step still owes
+    if (defer_fin(H) && (!H.df_mixed || jvp)) {
+      // the finalize the loop's last v-step still owes (full: its partials in
+      // part2; mixed jvp: the last F' step's, in part; mixed vjp owes none)
       StepArgs su, sv;
       FinArgs fu, fv;
       iter_args(H, jvp, su, sv, fu, fv);
+      fv.part = H.df_mixed ? W.part : W.part2;
+      fin_ptrs(H, fv);
       launch_df_tail(H, M, fv, st);
     }
     lsmr_flush(H, M, jvp, st);

@@ -101,6 +101,7 @@ struct Handle {
   int32_t *d_ft_order = nullptr;  // F' CTA -> unit order, PSD units first (null: natural order)
   int n_psd_units = 0;            // leading PSD units of d_ft_order (their own F' kernel, k_step_psd)
   bool defer_fin = false;       // single-problem graph loop with the deferred finalize (kFeatDF)
+  bool df_mixed = false;        // (PSD blocks: only the F step defers)
   int max_unit_rows = 0;         // rows of the longest work unit (kFeatDF staging)
   bool psd_split = true;         // QG_PSD_SPLIT at creation (0: PSD units stay in k_step, A/B)
   double *q = nullptr, *b = nullptr, *xbar = nullptr, *ybar = nullptr, *sbar = nullptr;

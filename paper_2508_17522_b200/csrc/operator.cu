@@ -975,7 +975,7 @@ __device__ void df_fin(const Mats &M, const StepArgs &a) {
     P.upd = L->itn > 0 ? 1 : 0;
     P.c_hbar = L->c_hbar; P.c_x = L->c_x; P.c_h = L->c_h; P.s_v = L->s_v;
     D->pub[par] = P;
-    D->pend_phase = a.is_v_step ? PH_STEP_V : PH_STEP_U;  // this step's finalize is owed to the next
+    D->pend_phase = a.df_next;  // the finalize owed to the next kFeatDF step
     __threadfence();
     st_release_u32(&D->flag[par], __ldcg(&D->flag[par ^ 1]) + 1);
   }
@@ -1042,16 +1042,13 @@ void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long c
 // opt == 0 the reference default 20 (n + m + 1) (lsmr.py:69-70 on the
 // embedding).  Thread 0 also arms the device-terminated loop: [0, cap].
 __global__ void k_init_state(Lsmr *st, int B, double atol, double btol, long long opt, const int64_t *xoff,
-                             const int64_t *yoff, long long *loop, long long cap, DfCtl *df) {
+                             const int64_t *yoff, long long *loop, long long cap) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p == 0 && loop) {
     loop[0] = 0;
     loop[1] = cap;
   }
-  if (p == 0 && df) {  // deferred-finalize loops start with nothing owed, publication counters at 0
-    df->flag[0] = df->flag[1] = 0;
-    df->pend_phase = 0;
-  }
+
   if (p >= B) return;
   Lsmr L{};
   L.atol = atol;
@@ -1260,10 +1257,13 @@ static void launch_step_one(const Handle &H, const Mats &M0, int kind, const Ste
 }
 
 void fin_ptrs(const Handle &H, FinArgs &a) {
-  // every producer writes one slot per work unit: X units, then Y units
-  a.px = H.ws.part;
+  // every producer writes one slot per work unit: X units, then Y units, in
+  // the buffer a.part (the workspace's part, or part2 for the steps of a
+  // deferred-finalize loop that write there)
+  const double *base = a.part ? a.part : H.ws.part;
+  a.px = base;
   a.px_ptr = H.d_xunit_ptr;
-  a.py = H.ws.part + (size_t)H.nxu() * kSlots;
+  a.py = base + (size_t)H.nxu() * kSlots;
   a.py_ptr = H.d_yunit_ptr;
 }
 
@@ -1302,19 +1302,23 @@ void launch_count_active(const Handle &H, cudaStream_t st) {
   QG_LAUNCHED();
 }
 
-void launch_df_tail(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t st) {
-  FinArgs a = a0;
-  a.px = H.ws.part2;  // the v-step's partials
-  a.px_ptr = H.d_xunit_ptr;
-  a.py = H.ws.part2 + (size_t)H.nxu() * kSlots;
-  a.py_ptr = H.d_yunit_ptr;
-  k_df_tail<<<1, 256, 0, st>>>(M, a, H.ws.df);
+void launch_df_tail(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st) {
+  k_df_tail<<<1, 256, 0, st>>>(M, a, H.ws.df);  // (a carries the owing step's partial-sum buffers)
+  QG_LAUNCHED();
+}
+
+__global__ void k_init_df(DfCtl *df, int pend) {
+  df->flag[0] = df->flag[1] = 0;
+  df->pend_phase = pend;
+}
+
+void launch_init_df(const Handle &H, int pend, cudaStream_t st) {
+  k_init_df<<<1, 1, 0, st>>>(H.ws.df, pend);
   QG_LAUNCHED();
 }
 
 void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st) {
-  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, opt, H.d_xoff, H.d_yoff, H.ws.d_loop, cap,
-                                                  H.ws.df);
+  k_init_state<<<(H.B + 127) / 128, 128, 0, st>>>(H.ws.st, H.B, atol, btol, opt, H.d_xoff, H.d_yoff, H.ws.d_loop, cap);
   QG_LAUNCHED();
 }
 

@@ -70,7 +70,8 @@ struct StepArgs {
   unsigned long long *prof = nullptr;  // QG_PSD_PROF diagnostics (qg_time_kernel): PSD unit phase cycles
   // deferred finalize (kFeatDF launches: CTA 0 finalizes, units from blockIdx 1)
   DfCtl *df = nullptr;
-  int df_par = 0;   // this step's publication slot (u-step 0, v-step 1)
+  int df_par = 0;   // this step's publication slot (alternates between successive kFeatDF steps)
+  int df_next = 0;  // the finalize owed to the next kFeatDF step after this one (its phase; 0: none)
   FinArgs fin{};    // the previous step's finalize (its partial sums in the other part buffer)
 };
 
@@ -91,6 +92,7 @@ void launch_update(const Handle &H, const Mats &M, const UpdArgs &a, cudaStream_
 void launch_count_active(const Handle &H, cudaStream_t st);
 void launch_init_state(const Handle &H, double atol, double btol, long long opt, long long cap, cudaStream_t st);
 void launch_df_tail(const Handle &H, const Mats &M, const FinArgs &a, cudaStream_t st);  // owed finalize after the loop
+void launch_init_df(const Handle &H, int pend, cudaStream_t st);  // arm the deferred-finalize control block
 void launch_engine(Handle &H, const Mats &M, bool jvp, cudaStream_t st);
 void launch_loop_cond(const Handle &H, cudaGraphConditionalHandle h, long long chunk, cudaStream_t st);
 

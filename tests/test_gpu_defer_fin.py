@@ -105,3 +105,51 @@ def test_defer_fin_launch_count(monkeypatch, c2):
         _run(b, dirs, atol=0.0, btol=0.0, max_iter=80)
         counts[f] = (_native.kernel_launches() - n1) - (n1 - n0)   # launches of 2 x 40 extra iterations
     assert counts["1"] == 2 * 2 * 40 + 2 * 40 // 4 and counts["0"] == 2 * 4 * 40 + 2 * 40 // 4, counts
+
+
+@pytest.fixture(scope="module")
+def c4s():
+    # c4's cone mix at 1/8 of its PSD blocks (nonneg + 64 x PSD(32)), diagonal P
+    cones = [("nonneg", 1250, 0, 0)] + [("psd", 528, 32, 0)] * 64
+    bt = synth.custom(cones, n=2500, nnzA=250_000, seed=31, diag_P=True)
+    return bt, synth.directions(bt, seed=32)
+
+
+def test_mixed_defer_fin_psd(monkeypatch, c4s):
+    """PSD blocks (the F' step split into k_step + k_step_psd): only the F step
+    defers -- its CTA 0 runs the F' step's finalize, a k_fin_cta the F step's
+    own (3 launches + the PSD branch per iteration).  Against the finalize-
+    kernel loop on the same work units at stable caps, the oracle, repeats."""
+    bt, dirs = c4s
+    monkeypatch.setenv("QG_TARGET_NNZ", "2048")
+    monkeypatch.setenv("QG_DEFER_FIN", "1")
+    b1 = _batch(bt)
+    monkeypatch.setenv("QG_DEFER_FIN", "0")
+    b0 = _batch(bt)
+    for K in (2, 5):
+        kw = dict(atol=0.0, btol=0.0, max_iter=K)
+        r1, r0 = _run(b1, dirs, **kw), _run(b0, dirs, **kw)
+        assert [d.iterations for d in r1[2] + r1[3]] == [K, K]
+        for a, c in zip(r1[0] + r1[1], r0[0] + r0[1]):
+            assert gap(a, c) <= 1e-9, K
+    th, sol, pert, de = cpu_bench.problem(bt, dirs, 0)
+    runs = OracleRuns(th, sol, pert, de).stable_caps((2, 5, 10))
+    assert runs, "no stable cap"
+    for K, (j0, v0) in runs.items():
+        jv = _run(b1, dirs, atol=0.0, btol=0.0, max_iter=K)
+        assert gap(np.concatenate(jv[0]), j0) <= 1e-6 and gap(np.concatenate(jv[1]), v0) <= 1e-6, K
+    a1 = _run(b1, dirs, atol=0.0, btol=0.0, max_iter=12)
+    a2 = _run(b1, dirs, atol=0.0, btol=0.0, max_iter=12)
+    for x, y in zip(a1[0] + a1[1], a2[0] + a2[1]):
+        assert np.array_equal(x, y)
+    # converged runs agree with the finalize-kernel loop on iterations and flags
+    c1, c0 = _run(b1, dirs), _run(b0, dirs)
+    for d1, d0 in zip(c1[2] + c1[3], c0[2] + c0[3]):
+        assert abs(d1.iterations - d0.iterations) <= max(3, d0.iterations // 50)
+        assert d1.converged == d0.converged
+    # launches: F (+ CTA 0), k_fin_cta, F' main + k_step_psd per iteration
+    n0 = _native.kernel_launches()
+    _run(b1, dirs, atol=0.0, btol=0.0, max_iter=40)
+    n1 = _native.kernel_launches()
+    _run(b1, dirs, atol=0.0, btol=0.0, max_iter=80)
+    assert (_native.kernel_launches() - n1) - (n1 - n0) == 2 * 4 * 40 + 2 * 40 // 4
