@@ -1206,8 +1206,24 @@ static void launch_step_main(const Handle &H, const Mats &M, int kind, const Ste
     grid += 1;
     const size_t stg = (size_t)2 * H.max_unit_rows * sizeof(double);
     (void)feat;  // (deferred-finalize handles have no CTA-per-row units: api.cu)
-    if (kind == STEP_F) go(k_step<STEP_F, 12, kFeatDF>, stg);
-    else go(k_step<STEP_FT, 12, kFeatDF>, stg);
+    // 8 CTAs/SM (64 registers: fewer spills) when the launch still fits in
+    // one wave, else 12: unit CTAs waiting for CTA 0 must not hold back a
+    // second wave (c2 30.1 -> 29.1, c4 99.8 -> 98.6 us per iteration with 8;
+    // c3's 1194 CTAs at 8 per SM: 47.9 -> 62.6, so it keeps 12)
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      QG_CUDA(cudaGetDevice(&dev));
+      QG_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const bool one_wave8 = grid <= 8u * (unsigned)nsm;
+    if (kind == STEP_F) {
+      if (one_wave8) go(k_step<STEP_F, 8, kFeatDF>, stg);
+      else go(k_step<STEP_F, 12, kFeatDF>, stg);
+    } else {
+      if (one_wave8) go(k_step<STEP_FT, 8, kFeatDF>, stg);
+      else go(k_step<STEP_FT, 12, kFeatDF>, stg);
+    }
     QG_LAUNCHED();
     return;
   }
