@@ -848,7 +848,7 @@ __device__ __forceinline__ void fin_cta_run(const Mats &M, const FinArgs &a, int
   if (!early && Lsh)
     for (int w = threadIdx.x; w < kLw; w += blockDim.x) sLw[w] = Lg[w];
   if (fin_skips(a, p)) return;  // CTA-uniform
-  __shared__ double red[(256 / 32) * 2 * kSlots];
+  __shared__ double red[(1024 / 32) * 2 * kSlots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (int)(blockDim.x >> 5);
   double s[2 * kSlots] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll 4
@@ -882,7 +882,8 @@ __device__ __forceinline__ void fin_cta_run(const Mats &M, const FinArgs &a, int
   }
 }
 
-__global__ void __launch_bounds__(256) k_fin_cta(Mats M, FinArgs a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_fin_cta(Mats M, FinArgs a) {
   const int p = (int)blockIdx.x;
   // the LSMR state goes to shared memory in one coalesced sweep (the scalar
   // recurrence then never waits on global memory for it), and back at the end
@@ -1301,7 +1302,11 @@ void launch_fin(const Handle &H, const Mats &M, const FinArgs &a0, cudaStream_t 
   // QG_FIN_CTA=0|1 forces (A/B).
   static const char *env = std::getenv("QG_FIN_CTA");
   const bool cta = !H.comm && (env ? std::atoi(env) != 0 : (int64_t)(H.nxu() + H.nyu()) >= 64LL * H.B);
-  if (cta) launch_pdl(k_fin_cta, dim3((unsigned)H.B), dim3(256), 0, st, M, a);
+  // (problems of >= 2048 units -- c5b, ~12k -- sum their partials with 1024
+  // threads: 4x fewer dependent load batches per thread)
+  if (cta && (int64_t)(H.nxu() + H.nyu()) >= 2048LL * H.B)
+    launch_pdl(k_fin_cta<1024>, dim3((unsigned)H.B), dim3(1024), 0, st, M, a);
+  else if (cta) launch_pdl(k_fin_cta<256>, dim3((unsigned)H.B), dim3(256), 0, st, M, a);
   else launch_pdl(k_fin, dim3(grid), dim3(256), 0, st, M, a);
   QG_LAUNCHED();
 }
